@@ -1,0 +1,229 @@
+/* wcgh.h — C ABI of the B200-native Fresnel hot path (sm_100a CUDA kernels).
+ *
+ * Drop-in boundary for the reference wavecgh 0.1.0 hot path
+ * (/root/reference/proj). The reference has no C ABI, plugin registry or FFI;
+ * its "operator API" is the set of C++ free functions listed beside each
+ * entry point below. Those functions keep their names, argument meaning and
+ * error behaviour in the host mirrors above this ABI (Python:
+ * paper_2211_09938_b200/wavecgh.py; C++: include/wavecgh_b200.hpp) and call
+ * these entry points, which launch the kernels. There is no CPU fallback: a
+ * missing device or a CUDA failure returns WCGH_ERUNTIME.
+ *
+ * Conventions
+ *  - Every call returns WCGH_OK (0), WCGH_EVALIDATION (1, the reference's
+ *    ValidationError, errors.hpp:10-13, CLI exit 1) or WCGH_ERUNTIME (2, the
+ *    IoError class, errors.hpp:17-20, CLI exit 2). No C++ exception crosses
+ *    the ABI; the message is in wcgh_last_error().
+ *  - Buffers are caller-owned. Unless a name ends in _dev, pointers are HOST
+ *    pointers (pinned or pageable) and calls are synchronous: results are
+ *    complete on return. Device memory is owned by the context / job.
+ *  - All images are square and row-major. Complex outputs are interleaved
+ *    float32 (re, im) = complex64, the CGHL/CGH1 payload layout
+ *    (fringe_lut.cpp:107-113, image_io.cpp:220-242).
+ *  - One context per GPU and host thread (one process per GPU). `workers`
+ *    arguments of the reference have no counterpart: results are bitwise
+ *    independent of the launch configuration and of the row-band split, the
+ *    GPU analogue of accumulate_deterministic (parallel.hpp:163-171).
+ */
+#ifndef WCGH_H
+#define WCGH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WCGH_ABI_VERSION 1
+
+enum { WCGH_OK = 0, WCGH_EVALIDATION = 1, WCGH_ERUNTIME = 2 };
+
+/* Input sample types. U8 objects are amplitudes v * obj_scale; U8 saliency is
+ * v * (1/255), the reference loader's scale_to_unit (image_io.cpp:177-190). */
+enum { WCGH_U8 = 0, WCGH_F32 = 1, WCGH_F64 = 2 };
+
+/* Synthesis method. DIRECT evaluates Eq.(1) per (point, pixel) on the SFU
+ * (tests/support/oracles.cpp:12-36 applied to the effective amplitude);
+ * LUT is the reference's production block-LUT superposition
+ * (synthesis.cpp:18-42, 55-69) for block sizes 8/4/2/1. */
+enum { WCGH_METHOD_DIRECT = 0, WCGH_METHOD_LUT = 1 };
+
+/* Phase evaluation for DIRECT. FIXED: exact 0.64 fixed-point quadratic phase
+ * frac(s * p^2/(2 lambda z)) + fp32 higher-order correction; FP64: r and
+ * k*r in double, then fp32 sin/cos of the reduced phase. */
+enum { WCGH_PHASE_FIXED = 0, WCGH_PHASE_FP64 = 1 };
+
+/* Operator levels, OpLevel (field.hpp:114-120). */
+enum { WCGH_OP_BASE_LLL = 0, WCGH_OP_REFINE_LL, WCGH_OP_REFINE_L, WCGH_OP_REFINE_FULL,
+       WCGH_OP_POINTWISE_ORACLE, WCGH_OP_LEVELS };
+
+/* One depth layer: SceneParams (field.hpp:91-108) minus plane_size. */
+typedef struct {
+  double wavelength; /* m */
+  double pitch;      /* m per pixel (object and hologram share the grid) */
+  double z;          /* m, object layer to hologram distance */
+} wcgh_layer;
+
+/* RefinementPlan (synthesis.hpp:18-29). */
+typedef struct {
+  double t_ll, t_l, t_full;
+  int enable_ll, enable_l, enable_full;
+} wcgh_plan;
+
+/* Compacted effective-amplitude point: hologram-grid coordinates (object
+ * offset applied), amplitude, depth layer. 16 bytes, the record the
+ * accumulation kernel stages through shared memory. */
+typedef struct {
+  int32_t x, y;
+  float a;
+  int32_t layer;
+} wcgh_point;
+
+/* A hologram job: n_layers objects of object_size^2 samples centred on a
+ * plane_size^2 hologram (offset (plane_size - object_size)/2, a multiple of
+ * 8 so Haar cells align with the reference's zero-padded run), of which this
+ * context computes rows [row0, row0 + rows). */
+typedef struct {
+  int object_size;  /* No: multiple of 8 */
+  int plane_size;   /* Nh: power of two >= No */
+  int n_layers;     /* 1..16 */
+  const wcgh_layer* layers;
+  wcgh_plan plan;
+  int method;       /* WCGH_METHOD_* */
+  int phase_mode;   /* WCGH_PHASE_* */
+  int row0, rows;   /* row band; rows = plane_size for a whole hologram */
+  int obj_dtype;    /* WCGH_U8 / WCGH_F32 / WCGH_F64 */
+  double obj_scale; /* amplitude = sample * obj_scale */
+  int sal_dtype;    /* WCGH_U8 / WCGH_F32 / WCGH_F64 */
+} wcgh_desc;
+
+/* Statistics of the last wcgh_job_run. */
+typedef struct {
+  uint64_t ops[WCGH_OP_LEVELS]; /* summed over layers */
+  int64_t n_points;             /* compacted nonzero A_eff points (direct) */
+  double updates;               /* algorithmic updates of the synthesis kernel */
+  float ms_analysis;            /* device time: DWT + gate + compaction */
+  float ms_synthesis;           /* device time: accumulation kernel(s) */
+  float ms_reduce;              /* device time: chunk reduction */
+  float ms_total;               /* device time of the whole run */
+  int synth_launches;           /* kernel launches of the synthesis step */
+  int total_launches;           /* all kernel launches of the run */
+} wcgh_stats;
+
+typedef struct wcgh_ctx wcgh_ctx;
+typedef struct wcgh_job wcgh_job;
+
+/* ---- context ----------------------------------------------------------- */
+int wcgh_abi_version(void);
+/* Creates a context on CUDA device `device`. */
+int wcgh_create(int device, wcgh_ctx** out);
+void wcgh_destroy(wcgh_ctx* ctx);
+/* Last error message of this thread (ctx may be NULL). */
+const char* wcgh_last_error(const wcgh_ctx* ctx);
+/* Runs all work of this context on `stream` (a cudaStream_t; NULL = the
+ * context's own stream). */
+int wcgh_set_stream(wcgh_ctx* ctx, void* stream);
+/* Number of SMs and the device name, for reporting. */
+int wcgh_device_info(wcgh_ctx* ctx, int* sm_count, char* name, int name_len);
+
+/* ---- stage entry points (host buffers; parity tests, C++/Python mirrors) --
+ *
+ * Replaces haar_analyze (haar.hpp:36, haar.cpp:52-74). pyramid layout: approx
+ * (n>>levels)^2, then per level l = 0..levels-1 (finest first) h, v, d each
+ * (n>>(l+1))^2, as doubles. Arithmetic is fp64 in the reference's order, so
+ * the bands are bit-identical to the reference for any input. */
+int wcgh_haar_analyze(wcgh_ctx* ctx, const void* image, int dtype, double scale, int n,
+                      int levels, double* pyramid);
+
+/* Replaces expand_residual (haar.hpp:46-47, haar.cpp:88-96): m x m -> (2m)^2. */
+int wcgh_expand_residual(wcgh_ctx* ctx, const double* h, const double* v, const double* d,
+                         int m, double* out);
+
+/* Replaces quantize_saliency (saliency.hpp:78, saliency.cpp:41-61): half,
+ * quarter, eighth block-max maps (doubles); validates [0,1] and n % 8. */
+int wcgh_quantize_saliency(wcgh_ctx* ctx, const void* saliency, int dtype, int n,
+                           double* sal_pyr);
+
+/* Analysis half of synthesize_progressive (synthesis.cpp:216-251) for one
+ * layer of n x n: gates (strict '>', synthesis.cpp:107-119), operator counts
+ * (synthesis.cpp:68), gated cell lists (row-major ascending y*m+x), the
+ * effective amplitude A_eff and its order-preserving compaction. Every output
+ * may be NULL. cells: concatenated ll, l, full lists (capacity (n/4)^2 +
+ * (n/2)^2 + n^2); cell_counts[3]. points: capacity n^2, coordinates offset by
+ * `offset`. */
+typedef struct {
+  double* pyramid;      /* 3-level layout of wcgh_haar_analyze */
+  double* sal_pyr;      /* half, quarter, eighth */
+  uint8_t* masks;       /* mask_ll (n/4)^2, mask_l (n/2)^2, mask_full n^2 */
+  float* a_eff;         /* n^2 */
+  uint32_t* cells;      /* gated cells per stage */
+  int64_t cell_counts[3];
+  wcgh_point* points;   /* compacted A_eff */
+  int64_t n_points;
+  uint64_t ops[WCGH_OP_LEVELS];
+} wcgh_analysis;
+int wcgh_analyze(wcgh_ctx* ctx, const void* object, int obj_dtype, double obj_scale,
+                 const void* saliency, int sal_dtype, int n, const wcgh_plan* plan,
+                 int offset, int layer, wcgh_analysis* out);
+
+/* Direct Eq.(1) accumulation of a host point list over hologram rows
+ * [row0, row0+rows) of an nh-wide plane: out = rows x nh complex64.
+ * Points must be sorted by layer. The exact sum the reference's
+ * pointwise_sum forms (tests/support/oracles.cpp:12-36), per layer z. */
+int wcgh_synth_points(wcgh_ctx* ctx, const wcgh_point* points, int64_t n_points,
+                      const wcgh_layer* layers, int n_layers, int nh, int row0, int rows,
+                      int phase_mode, float* out);
+
+/* Replaces build_block_lut (fringe_lut.hpp:126, fringe_lut.cpp:53-93) on the
+ * GPU: the (2n-1)^2 support of a B x B block, summed in fp64 and stored as
+ * complex64 (the CGHL payload, fringe_lut.cpp:107-113). */
+int wcgh_build_block_lut(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int block, float* out);
+
+/* Replaces apply_block (synthesis.hpp:68-69, synthesis.cpp:149-160) for a
+ * batch: plane (n x n complex64, in/out) += sum_i w_i * crop(S_B at cell_i),
+ * with S_B built on the device for `scene`. cells are y*m+x on the m = n/B
+ * grid; zero weights add nothing but count (ops_out += n_cells). */
+int wcgh_apply_blocks(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int block,
+                      const uint32_t* cells, const float* weights, int64_t n_cells,
+                      float* plane, uint64_t* ops_out);
+
+/* Replaces refine (synthesis.hpp:79-82, synthesis.cpp:90-123 + 171-178):
+ * expands (h, v, d) (m x m each) into the 2m x 2m residual, gates it with
+ * saliency_finer (2m x 2m, doubles) by the strict '>' against `threshold`,
+ * and adds the block-B LUT contribution of every gated cell to `plane`
+ * (n x n complex64, in/out), where B = n / (2m). mask_out (2m x 2m bytes)
+ * may be NULL; ops_out += number of gated cells. */
+int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, const double* v,
+                const double* d, int m, const double* saliency_finer, double threshold,
+                float* plane, uint8_t* mask_out, uint64_t* ops_out);
+
+/* ---- jobs: resident inputs, device-side hologram ------------------------ */
+int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out);
+void wcgh_job_destroy(wcgh_job* job);
+/* H2D of n_layers x No^2 object and saliency samples (layer-major). */
+int wcgh_job_upload(wcgh_job* job, const void* object, const void* saliency);
+/* Same from device pointers (device-to-device copy). */
+int wcgh_job_upload_dev(wcgh_job* job, const void* object_dev, const void* saliency_dev);
+/* Analysis + compaction + synthesis of the row band into the job's device
+ * plane. Returns after the work is enqueued AND complete (synchronous). */
+int wcgh_job_run(wcgh_job* job);
+/* D2H of the row band: rows x Nh complex64. */
+int wcgh_job_download(wcgh_job* job, float* out);
+/* Stage snapshots of the last run (LUT method): base_LLL, after_LL,
+ * after_L, after_full (synthesis.hpp:43-54), each rows x Nh complex64. */
+int wcgh_job_download_stages(wcgh_job* job, float* out4);
+/* Device pointer of the row band (rows x Nh complex64), valid until destroy. */
+void* wcgh_job_plane_dev(wcgh_job* job);
+int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out);
+
+/* One-shot: job create + upload + run + download + destroy. The entry the
+ * C++ synthesize_progressive mirror calls (synthesis.hpp:88-91). */
+int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object,
+                    const void* saliency, float* out, wcgh_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WCGH_H */

@@ -1,0 +1,55 @@
+"""In-tree build of libwcgh.so (sm_100a) with nvcc.
+
+The shared library lands next to this file so it travels with the repo
+snapshot to the GPU box; no JIT cache is involved.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = ROOT / "build" / "wcgh"
+LIB = PKG / "libwcgh.so"
+SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_abi.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+         "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
+
+
+def _run(cmd: list[str], log: Path | None = None) -> None:
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        log.write_text(res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd)}")
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    BUILD.mkdir(parents=True, exist_ok=True)
+    deps = [CSRC / s for s in SOURCES] + [CSRC / "wcgh_internal.cuh", ROOT / "include" / "wcgh.h"]
+    newest = max(p.stat().st_mtime for p in deps)
+    if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
+        return LIB
+    objs = []
+    for src in SOURCES:
+        obj = BUILD / (Path(src).stem + ".o")
+        _run([NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)],
+             log=BUILD / (Path(src).stem + ".ptxas.log"))
+        objs.append(str(obj))
+        if verbose:
+            print((BUILD / (Path(src).stem + ".ptxas.log")).read_text())
+    tmp = LIB.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    tmp.replace(LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

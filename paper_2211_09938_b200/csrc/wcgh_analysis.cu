@@ -1,0 +1,581 @@
+// K1 + K2: warp-shuffle 3-level Haar DWT, saliency block-max, strict gates,
+// effective amplitude A_eff, operator counts, and order-preserving
+// compaction of the nonzero A_eff samples into point records.
+//
+// Reference semantics restated (paths under /root/reference/proj):
+//   analyze_level        core/src/haar.cpp:12-30   (fp64, same operation order)
+//   haar_analyze         core/src/haar.cpp:52-74   (details[0] finest)
+//   synthesize_level     core/src/haar.cpp:32-48   (expand_residual, a = 0.0)
+//   block_max            core/src/saliency.cpp:12-26
+//   quantize_saliency    core/src/saliency.cpp:41-61 ([0,1] check)
+//   gate loop            core/src/synthesis.cpp:107-119 (strict '>')
+//   op counts            core/src/synthesis.cpp:68, 77-88 (base = every LLL cell)
+//   A_eff identity       SURVEY.md §0 finding 1: after_full == pointwise_sum(A_eff)
+//
+// Thread mapping: one thread per level-1 quad (2x2 pixels). A warp covers
+// 8 x 4 quads (16 x 8 pixels = two LLL cells); level 2 combines lanes
+// {l, l^1, l^8, l^9}, level 3 lanes {b, b+2, b+16, b+18}, all by shuffles.
+// A CTA of 8 warps covers a 128 x 8 pixel strip. Everything is computed in
+// fp64 so the bands are bit-identical to the reference for any input; A_eff
+// is rounded to fp32 once, at the end.
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "wcgh_internal.cuh"
+
+namespace wcgh {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T>
+__device__ __forceinline__ double load_obj(const T* p, size_t i, double scale);
+template <>
+__device__ __forceinline__ double load_obj<uint8_t>(const uint8_t* p, size_t i, double scale) {
+  return double(p[i]) * scale;
+}
+template <>
+__device__ __forceinline__ double load_obj<float>(const float* p, size_t i, double scale) {
+  return double(p[i]) * scale;
+}
+template <>
+__device__ __forceinline__ double load_obj<double>(const double* p, size_t i, double scale) {
+  return p[i] * scale;
+}
+
+// Saliency to double: u8 is v * (1/255) like scale_to_unit (image_io.cpp:177-190).
+template <typename T>
+__device__ __forceinline__ double load_sal(const T* p, size_t i);
+template <>
+__device__ __forceinline__ double load_sal<uint8_t>(const uint8_t* p, size_t i) {
+  return double(p[i]) * (1.0 / 255.0);
+}
+template <>
+__device__ __forceinline__ double load_sal<float>(const float* p, size_t i) {
+  return double(p[i]);
+}
+template <>
+__device__ __forceinline__ double load_sal<double>(const double* p, size_t i) {
+  return p[i];
+}
+
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(kFull, v, src); }
+
+// std::max(best, v) with best starting at 0.0 (saliency.cpp:19-22).
+__device__ __forceinline__ double dmax(double best, double v) { return best < v ? v : best; }
+
+// One averaging analysis step (haar.cpp:20-27), reference operation order.
+struct Quad {
+  double a, h, v, d;
+};
+__device__ __forceinline__ Quad analyze4(double c00, double c01, double c10, double c11) {
+  Quad q;
+  q.a = (c00 + c01 + c10 + c11) * 0.25;
+  q.h = (c00 - c01 + c10 - c11) * 0.25;
+  q.v = (c00 + c01 - c10 - c11) * 0.25;
+  q.d = (c00 - c01 - c10 + c11) * 0.25;
+  return q;
+}
+
+// synthesize_level with av = 0.0 (haar.cpp:37-44) at child (sx, sy).
+__device__ __forceinline__ double expand_at(double h, double v, double d, int sx, int sy) {
+  const double av = 0.0;
+  if (sy == 0) return sx == 0 ? av + h + v + d : av - h + v - d;
+  return sx == 0 ? av + h - v - d : av - h - v + d;
+}
+
+template <typename TO, typename TS>
+__global__ void __launch_bounds__(256) k_analysis(const TO* __restrict__ obj, double obj_scale,
+                                                  const TS* __restrict__ sal, int n,
+                                                  wcgh_plan plan, AnalysisOut out) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int layer = blockIdx.z;
+  const size_t n2 = size_t(n) * n;
+  obj += layer * n2;
+  sal += layer * n2;
+
+  const int qx = blockIdx.x * 64 + warp * 8 + (lane & 7);  // quad column
+  const int qy = blockIdx.y * 4 + (lane >> 3);             // quad row
+  const int m1 = n / 2;
+  const bool valid = qx < m1;
+  const int px = 2 * qx, py = 2 * qy;
+
+  double c00 = 0, c01 = 0, c10 = 0, c11 = 0, s00 = 0, s01 = 0, s10 = 0, s11 = 0;
+  int err = 0;
+  if (valid) {
+    const size_t r0 = size_t(py) * n + px, r1 = r0 + n;
+    c00 = load_obj(obj, r0, obj_scale);
+    c01 = load_obj(obj, r0 + 1, obj_scale);
+    c10 = load_obj(obj, r1, obj_scale);
+    c11 = load_obj(obj, r1 + 1, obj_scale);
+    s00 = load_sal(sal, r0);
+    s01 = load_sal(sal, r0 + 1);
+    s10 = load_sal(sal, r1);
+    s11 = load_sal(sal, r1 + 1);
+    if (!(isfinite(c00) && isfinite(c01) && isfinite(c10) && isfinite(c11))) err |= kErrObjectNonFinite;
+    if (!(s00 >= 0.0 && s00 <= 1.0 && s01 >= 0.0 && s01 <= 1.0 && s10 >= 0.0 && s10 <= 1.0 &&
+          s11 >= 0.0 && s11 <= 1.0))
+      err |= kErrSaliencyRange;
+  }
+
+  // Level 1 (details[0], n/2 grid).
+  const Quad q1 = analyze4(c00, c01, c10, c11);
+  double s1 = dmax(dmax(dmax(dmax(0.0, s00), s01), s10), s11);
+
+  // Level 2 (details[1], n/4 grid): quads (2X,2Y),(2X+1,2Y),(2X,2Y+1),(2X+1,2Y+1).
+  const int b2 = lane & ~(1 | 8);
+  const Quad q2 = analyze4(shfl(q1.a, b2), shfl(q1.a, b2 + 1), shfl(q1.a, b2 + 8),
+                           shfl(q1.a, b2 + 9));
+  // block max over the 4x4 pixel block = max of the four quad maxima
+  double s2 = dmax(dmax(dmax(dmax(0.0, shfl(s1, b2)), shfl(s1, b2 + 1)), shfl(s1, b2 + 8)),
+                   shfl(s1, b2 + 9));
+
+  // Level 3 (details[2] and approx LLL, n/8 grid).
+  const int b3 = lane & 4;
+  const Quad q3 = analyze4(shfl(q2.a, b3), shfl(q2.a, b3 + 2), shfl(q2.a, b3 + 16),
+                           shfl(q2.a, b3 + 18));
+  const double s3 =
+      dmax(dmax(dmax(dmax(0.0, shfl(s2, b3)), shfl(s2, b3 + 2)), shfl(s2, b3 + 16)),
+           shfl(s2, b3 + 18));
+
+  // Gates (synthesis.cpp:112-118): stage LL on by_factor(4), L on
+  // by_factor(2), full on the full-resolution map; strict '>'.
+  const bool g_ll = plan.enable_ll && s2 > plan.t_ll;
+  const bool g_l = plan.enable_l && s1 > plan.t_l;
+  const bool gf00 = plan.enable_full && s00 > plan.t_full;
+  const bool gf01 = plan.enable_full && s01 > plan.t_full;
+  const bool gf10 = plan.enable_full && s10 > plan.t_full;
+  const bool gf11 = plan.enable_full && s11 > plan.t_full;
+
+  // Residuals at this thread's cells (expand_residual, haar.cpp:88-96).
+  const int x1 = lane & 1, y1 = (lane >> 3) & 1;         // quad inside its level-2 cell
+  const int x2 = (lane >> 1) & 1, y2 = (lane >> 4) & 1;  // level-2 cell inside its LLL cell
+  const double r_ll = expand_at(q3.h, q3.v, q3.d, x2, y2);
+  const double r_l = expand_at(q2.h, q2.v, q2.d, x1, y1);
+  const double rf00 = expand_at(q1.h, q1.v, q1.d, 0, 0);
+  const double rf01 = expand_at(q1.h, q1.v, q1.d, 1, 0);
+  const double rf10 = expand_at(q1.h, q1.v, q1.d, 0, 1);
+  const double rf11 = expand_at(q1.h, q1.v, q1.d, 1, 1);
+
+  // A_eff = up8(LLL) + g_ll*up4(r_ll) + g_l*up2(r_l) + g_full*r_full.
+  double base = q3.a;
+  if (g_ll) base += r_ll;
+  if (g_l) base += r_l;
+  double e00 = base, e01 = base, e10 = base, e11 = base;
+  if (gf00) e00 += rf00;
+  if (gf01) e01 += rf01;
+  if (gf10) e10 += rf10;
+  if (gf11) e11 += rf11;
+  const float f00 = float(e00), f01 = float(e01), f10 = float(e10), f11 = float(e11);
+
+  const bool lead2 = x1 == 0 && y1 == 0;     // one lane per level-2 cell
+  const bool lead3 = lead2 && x2 == 0 && y2 == 0;  // one lane per LLL cell
+  const int m2 = n / 4, m3 = n / 8;
+  const int qx2 = qx >> 1, qy2 = qy >> 1, qx3 = qx >> 2, qy3 = qy >> 2;
+
+  if (valid) {
+    const size_t r0 = size_t(py) * n + px;
+    float* ae = out.a_eff + layer * n2;
+    *reinterpret_cast<float2*>(ae + r0) = make_float2(f00, f01);
+    *reinterpret_cast<float2*>(ae + r0 + n) = make_float2(f10, f11);
+
+    if (out.masks) {
+      uint8_t* mk = out.masks + layer * masks_len(n);
+      uint8_t* mk_ll = mk;
+      uint8_t* mk_l = mk + size_t(m2) * m2;
+      uint8_t* mk_f = mk_l + size_t(m1) * m1;
+      mk_l[size_t(qy) * m1 + qx] = g_l;
+      mk_f[r0] = gf00;
+      mk_f[r0 + 1] = gf01;
+      mk_f[r0 + n] = gf10;
+      mk_f[r0 + n + 1] = gf11;
+      if (lead2) mk_ll[size_t(qy2) * m2 + qx2] = g_ll;
+    }
+    if (out.w_stage) {  // dense per-stage LUT weights (zero where gated out)
+      float* w = out.w_stage + layer * wstage_len(n);
+      float* w_base = w;
+      float* w_ll = w_base + size_t(m3) * m3;
+      float* w_l = w_ll + size_t(m2) * m2;
+      float* w_f = w_l + size_t(m1) * m1;
+      w_l[size_t(qy) * m1 + qx] = g_l ? float(r_l) : 0.0f;
+      *reinterpret_cast<float2*>(w_f + r0) =
+          make_float2(gf00 ? float(rf00) : 0.0f, gf01 ? float(rf01) : 0.0f);
+      *reinterpret_cast<float2*>(w_f + r0 + n) =
+          make_float2(gf10 ? float(rf10) : 0.0f, gf11 ? float(rf11) : 0.0f);
+      if (lead2) w_ll[size_t(qy2) * m2 + qx2] = g_ll ? float(r_ll) : 0.0f;
+      if (lead3) w_base[size_t(qy3) * m3 + qx3] = float(q3.a);
+    }
+    if (out.pyramid) {
+      // approx (n/8)^2, details[0] (h,v,d at n/2), details[1] (n/4), details[2] (n/8)
+      double* p = out.pyramid + layer * pyr_len(n);
+      const size_t e2 = size_t(m3) * m3, h2 = size_t(m1) * m1, q2s = size_t(m2) * m2;
+      double* d0 = p + e2;
+      double* d1 = d0 + 3 * h2;
+      double* d2 = d1 + 3 * q2s;
+      const size_t i1 = size_t(qy) * m1 + qx;
+      d0[i1] = q1.h;
+      d0[h2 + i1] = q1.v;
+      d0[2 * h2 + i1] = q1.d;
+      if (lead2) {
+        const size_t i2 = size_t(qy2) * m2 + qx2;
+        d1[i2] = q2.h;
+        d1[q2s + i2] = q2.v;
+        d1[2 * q2s + i2] = q2.d;
+      }
+      if (lead3) {
+        const size_t i3 = size_t(qy3) * m3 + qx3;
+        p[i3] = q3.a;
+        d2[i3] = q3.h;
+        d2[e2 + i3] = q3.v;
+        d2[2 * e2 + i3] = q3.d;
+      }
+    }
+    if (out.sal_pyr) {
+      double* sp = out.sal_pyr + layer * salpyr_len(n);
+      sp[size_t(qy) * m1 + qx] = s1;
+      if (lead2) sp[size_t(m1) * m1 + size_t(qy2) * m2 + qx2] = s2;
+      if (lead3) sp[size_t(m1) * m1 + size_t(m2) * m2 + size_t(qy3) * m3 + qx3] = s3;
+    }
+  }
+
+  // Operator counts: integer reductions, order-independent.
+  const unsigned vmask = __ballot_sync(kFull, valid);
+  const int c_ll = __popc(__ballot_sync(kFull, valid && lead2 && g_ll));
+  const int c_l = __popc(__ballot_sync(kFull, valid && g_l));
+  const int c_f = __popc(__ballot_sync(kFull, valid && gf00)) + __popc(__ballot_sync(kFull, valid && gf01)) +
+                  __popc(__ballot_sync(kFull, valid && gf10)) + __popc(__ballot_sync(kFull, valid && gf11));
+  const int c_base = __popc(__ballot_sync(kFull, valid && lead3));
+  const int anyerr = __reduce_or_sync(kFull, err);
+  if (lane == 0 && vmask) {
+    unsigned long long* ops = out.ops + layer * WCGH_OP_LEVELS;
+    if (c_base) atomicAdd(ops + WCGH_OP_BASE_LLL, (unsigned long long)c_base);
+    if (c_ll) atomicAdd(ops + WCGH_OP_REFINE_LL, (unsigned long long)c_ll);
+    if (c_l) atomicAdd(ops + WCGH_OP_REFINE_L, (unsigned long long)c_l);
+    if (c_f) atomicAdd(ops + WCGH_OP_REFINE_FULL, (unsigned long long)c_f);
+    if (anyerr) atomicOr(out.err, anyerr);
+  }
+
+  // Compaction counts: nonzero A_eff per (row, 128-pixel segment).
+  if (out.seg_counts) {
+    __shared__ int cnt[8];
+    if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int nz_top = valid ? int(f00 != 0.0f) + int(f01 != 0.0f) : 0;
+    const int nz_bot = valid ? int(f10 != 0.0f) + int(f11 != 0.0f) : 0;
+    // lanes sharing a quad row: lane>>3; reduce within the 8-lane group
+    int t = nz_top, b = nz_bot;
+    for (int o = 4; o; o >>= 1) {
+      t += __shfl_xor_sync(kFull, t, o);
+      b += __shfl_xor_sync(kFull, b, o);
+    }
+    if ((lane & 7) == 0) {
+      const int r = 2 * (lane >> 3);
+      if (t) atomicAdd(&cnt[r], t);
+      if (b) atomicAdd(&cnt[r + 1], b);
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      const int segs = seg_per_row(n);
+      const int row = blockIdx.y * 8 + threadIdx.x;
+      out.seg_counts[(size_t(layer) * n + row) * segs + blockIdx.x] = cnt[threadIdx.x];
+    }
+  }
+}
+
+// Single-CTA exclusive scan (counts are per row segment: at most a few
+// hundred thousand entries).
+__global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ counts, int* __restrict__ offsets,
+                                               int count) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < count; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < count ? counts[i] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = warp_sums[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int incl = x + (warp ? warp_sums[warp - 1] : 0) + carry;
+    if (i < count) offsets[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[count] = carry;
+}
+
+// Ordered compaction: one warp per (layer, row, 128-pixel segment); lane l
+// owns pixels 4l..4l+3 of the segment.
+__global__ void __launch_bounds__(256) k_compact_points(const float* __restrict__ a_eff,
+                                                        const int* __restrict__ offsets, int n,
+                                                        int n_layers, int off, int layer0,
+                                                        wcgh_point* __restrict__ points) {
+  const int lane = threadIdx.x & 31;
+  const int segs = seg_per_row(n);
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const long long total = (long long)n_layers * n * segs;
+  if (gw >= total) return;
+  const int seg = int(gw % segs);
+  const long long lr = gw / segs;
+  const int row = int(lr % n);
+  const int layer = int(lr / n);
+  const float* src = a_eff + (size_t(layer) * n + row) * n;
+  const int x0 = seg * 128 + 4 * lane;
+  float v[4];
+  int nz = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = (x0 + k < n) ? src[x0 + k] : 0.0f;
+    nz += v[k] != 0.0f;
+  }
+  int incl = nz;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int pos = offsets[gw] + incl - nz;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (v[k] != 0.0f) {
+      wcgh_point p;
+      p.x = x0 + k + off;
+      p.y = row + off;
+      p.a = v[k];
+      p.layer = layer0 + layer;
+      points[pos++] = p;
+    }
+  }
+}
+
+// Mask cell lists (row-major ascending y*m + x), same two-pass scheme.
+__global__ void k_mask_counts(const uint8_t* __restrict__ mask, int m, int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int segs = seg_per_row(m);
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gw >= (long long)m * segs) return;
+  const int seg = int(gw % segs), row = int(gw / segs);
+  int nz = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int x = seg * 128 + 4 * lane + k;
+    nz += (x < m) && mask[size_t(row) * m + x] != 0;
+  }
+  for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(kFull, nz, o);
+  if (lane == 0) counts[gw] = nz;
+}
+
+__global__ void k_compact_mask(const uint8_t* __restrict__ mask, int m, const int* __restrict__ offsets,
+                               uint32_t* __restrict__ cells) {
+  const int lane = threadIdx.x & 31;
+  const int segs = seg_per_row(m);
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gw >= (long long)m * segs) return;
+  const int seg = int(gw % segs), row = int(gw / segs);
+  bool on[4];
+  int nz = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int x = seg * 128 + 4 * lane + k;
+    on[k] = (x < m) && mask[size_t(row) * m + x] != 0;
+    nz += on[k];
+  }
+  int incl = nz;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int pos = offsets[gw] + incl - nz;
+  for (int k = 0; k < 4; ++k)
+    if (on[k]) cells[pos++] = uint32_t(row) * uint32_t(m) + uint32_t(seg * 128 + 4 * lane + k);
+}
+
+// One averaging analysis level for wcgh_haar_analyze with levels != 3
+// (haar.cpp:12-30): in n x n -> a, h, v, d each (n/2)^2.
+__global__ void k_analyze_level(const double* __restrict__ in, int n, double* __restrict__ a,
+                                double* __restrict__ h, double* __restrict__ v,
+                                double* __restrict__ d) {
+  const int m = n / 2;
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= size_t(m) * m) return;
+  const int x = int(i % m), y = int(i / m);
+  const size_t r0 = size_t(2 * y) * n + 2 * x;
+  const Quad q = analyze4(in[r0], in[r0 + 1], in[r0 + n], in[r0 + n + 1]);
+  a[i] = q.a;
+  h[i] = q.h;
+  v[i] = q.v;
+  d[i] = q.d;
+}
+
+template <typename T>
+__global__ void k_to_double(const T* __restrict__ in, size_t count, double scale,
+                            double* __restrict__ out, int* __restrict__ err) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double v = load_obj(in, i, scale);
+  if (!isfinite(v)) atomicOr(err, kErrObjectNonFinite);
+  out[i] = v;
+}
+
+// refine_stage gate (synthesis.cpp:107-119) fused with expand_residual: one
+// thread per band sample, writing the four residual cells it expands to.
+__global__ void k_refine_gate(const double* __restrict__ h, const double* __restrict__ v,
+                              const double* __restrict__ d, int m, const double* __restrict__ sal,
+                              double t, float* __restrict__ w, uint8_t* __restrict__ mask,
+                              unsigned long long* __restrict__ count) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int c = 0;
+  if (i < size_t(m) * m) {
+    const int x = int(i % m), y = int(i / m);
+    const int n = 2 * m;
+    for (int sy = 0; sy < 2; ++sy)
+      for (int sx = 0; sx < 2; ++sx) {
+        const size_t o = size_t(2 * y + sy) * n + 2 * x + sx;
+        const bool on = sal[o] > t;
+        w[o] = on ? float(expand_at(h[i], v[i], d[i], sx, sy)) : 0.0f;
+        if (mask) mask[o] = on;
+        c += on;
+      }
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+__global__ void k_expand_residual(const double* __restrict__ h, const double* __restrict__ v,
+                                  const double* __restrict__ d, int m, double* __restrict__ out) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= size_t(m) * m) return;
+  const int x = int(i % m), y = int(i / m);
+  const int n = 2 * m;
+  for (int sy = 0; sy < 2; ++sy)
+    for (int sx = 0; sx < 2; ++sx)
+      out[size_t(2 * y + sy) * n + 2 * x + sx] = expand_at(h[i], v[i], d[i], sx, sy);
+}
+
+template <typename TO, typename TS>
+void launch_k1(const void* obj, double scale, const void* sal, int n, int n_layers,
+               const wcgh_plan& plan, const AnalysisOut& out, cudaStream_t s) {
+  dim3 grid((n + 127) / 128, n / 8, n_layers);
+  k_analysis<TO, TS><<<grid, 256, 0, s>>>(static_cast<const TO*>(obj), scale,
+                                          static_cast<const TS*>(sal), n, plan, out);
+}
+
+template <typename TO>
+void dispatch_sal(const void* obj, double scale, const void* sal, int sal_dtype, int n, int L,
+                  const wcgh_plan& plan, const AnalysisOut& out, cudaStream_t s) {
+  switch (sal_dtype) {
+    case WCGH_U8: launch_k1<TO, uint8_t>(obj, scale, sal, n, L, plan, out, s); break;
+    case WCGH_F32: launch_k1<TO, float>(obj, scale, sal, n, L, plan, out, s); break;
+    case WCGH_F64: launch_k1<TO, double>(obj, scale, sal, n, L, plan, out, s); break;
+    default: throw ValidationError("saliency dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
+  }
+}
+
+}  // namespace
+
+int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void* sal,
+                    int sal_dtype, int n, int n_layers, const wcgh_plan& plan,
+                    const AnalysisOut& out, cudaStream_t s) {
+  require(n >= 8 && n % 8 == 0, "analysis: side must be a positive multiple of 8");
+  switch (obj_dtype) {
+    case WCGH_U8: dispatch_sal<uint8_t>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
+    case WCGH_F32: dispatch_sal<float>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
+    case WCGH_F64: dispatch_sal<double>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
+    default: throw ValidationError("object dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
+  }
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_scan(const int* counts, int* offsets, int count, cudaStream_t s) {
+  k_scan<<<1, 1024, 0, s>>>(counts, offsets, count);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers, int off,
+                          int layer0, wcgh_point* points, cudaStream_t s) {
+  const long long warps = (long long)n_layers * n * seg_per_row(n);
+  k_compact_points<<<unsigned((warps + 7) / 8), 256, 0, s>>>(a_eff, offsets, n, n_layers, off,
+                                                             layer0, points);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_mask_counts(const uint8_t* mask, int m, int* seg_counts, cudaStream_t s) {
+  const long long warps = (long long)m * seg_per_row(m);
+  k_mask_counts<<<unsigned((warps + 7) / 8), 256, 0, s>>>(mask, m, seg_counts);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_compact_mask(const uint8_t* mask, int m, const int* offsets, uint32_t* cells,
+                        cudaStream_t s) {
+  const long long warps = (long long)m * seg_per_row(m);
+  k_compact_mask<<<unsigned((warps + 7) / 8), 256, 0, s>>>(mask, m, offsets, cells);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_haar_levels(const void* image, int dtype, double scale, int n, int levels,
+                       double* pyramid, double* scratch, int* err, cudaStream_t s) {
+  const size_t n2 = size_t(n) * n;
+  // scratch: 2 * n2 doubles (current level + next approximation)
+  double* cur = scratch;
+  double* nxt = scratch + n2;
+  const unsigned g = unsigned((n2 + 255) / 256);
+  switch (dtype) {
+    case WCGH_U8: k_to_double<<<g, 256, 0, s>>>(static_cast<const uint8_t*>(image), n2, scale, cur, err); break;
+    case WCGH_F32: k_to_double<<<g, 256, 0, s>>>(static_cast<const float*>(image), n2, scale, cur, err); break;
+    case WCGH_F64: k_to_double<<<g, 256, 0, s>>>(static_cast<const double*>(image), n2, scale, cur, err); break;
+    default: throw ValidationError("dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
+  }
+  WCGH_CHECK_LAUNCH();
+  const int ma = n >> levels;
+  double* out = pyramid + size_t(ma) * ma;
+  int side = n;
+  for (int l = 0; l < levels; ++l) {
+    const int m = side / 2;
+    const size_t mm = size_t(m) * m;
+    k_analyze_level<<<unsigned((mm + 255) / 256), 256, 0, s>>>(cur, side, nxt, out, out + mm, out + 2 * mm);
+    WCGH_CHECK_LAUNCH();
+    out += 3 * mm;
+    std::swap(cur, nxt);
+    side = m;
+  }
+  WCGH_CUDA(cudaMemcpyAsync(pyramid, cur, sizeof(double) * size_t(ma) * ma, cudaMemcpyDeviceToDevice, s));
+  return levels + 1;
+}
+
+int launch_refine_gate(const double* h, const double* v, const double* d, int m,
+                       const double* sal, double t, float* w, uint8_t* mask,
+                       unsigned long long* count, cudaStream_t s) {
+  const size_t cnt = size_t(m) * m;
+  k_refine_gate<<<unsigned((cnt + 255) / 256), 256, 0, s>>>(h, v, d, m, sal, t, w, mask, count);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_expand_residual(const double* h, const double* v, const double* d, int m, double* out,
+                           cudaStream_t s) {
+  const size_t cnt = size_t(m) * m;
+  k_expand_residual<<<unsigned((cnt + 255) / 256), 256, 0, s>>>(h, v, d, m, out);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+}  // namespace wcgh

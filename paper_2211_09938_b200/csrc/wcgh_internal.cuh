@@ -1,0 +1,182 @@
+// Internal declarations shared by the wcgh CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/wcgh.h"
+
+namespace wcgh {
+
+// Error types mirroring the reference's ValidationError / IoError
+// (errors.hpp:10-20); mapped to WCGH_EVALIDATION / WCGH_ERUNTIME at the ABI.
+struct ValidationError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define WCGH_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::wcgh::RuntimeError(std::string("CUDA error ") + cudaGetErrorString(e_) +     \
+                                 " at " + __FILE__ + ":" + std::to_string(__LINE__));       \
+  } while (0)
+
+#define WCGH_CHECK_LAUNCH() WCGH_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string& what) {
+  if (!ok) throw ValidationError(what);
+}
+
+// RAII device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // Grows to at least n bytes (contents not preserved).
+  void* reserve(size_t n) {
+    if (n <= bytes && p) return p;
+    release();
+    if (n == 0) n = 16;
+    WCGH_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+    return p;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// ---- direct accumulation (K3) ---------------------------------------------
+
+constexpr int kMaxLayers = 16;
+constexpr int kMaxCorr = 8;  // phase-correction series terms b_2 .. b_9
+
+// Per-layer constants of the fixed-point phase evaluation. Total phase in
+// cycles: z/lambda * sqrt(1 + u), u = s p^2/z^2, s = dx^2 + dy^2, split as
+//   frac(z/lambda)  +  s * alpha  +  (z/lambda) * g(u),
+//   alpha = p^2 / (2 lambda z),  g(u) = sqrt(1+u) - 1 - u/2 = sum_{n>=2} C(1/2,n) u^n.
+// The first two are exact 32-/64-bit fixed point; g is an fp32 series.
+struct DirectLayer {
+  uint32_t a_hi, a_lo;   // frac(alpha) in 0.64 fixed point
+  uint32_t phi0;         // frac(z/lambda) in 0.32 fixed point
+  uint32_t dd;           // frac(2*32^2*alpha): second difference along a thread's pixels
+  float c;               // p^2 / z^2
+  float inv_z;           // 1/z
+  float corr[kMaxCorr];  // 2*pi*(z/lambda)*C(1/2, n+2): radians per u^(n+2)
+  float amp[4];          // C(-1/2, n+1): (1+u)^(-1/2) = 1 + sum amp[n] u^(n+1)
+  double wavelength, pitch, z, k;  // fp64 phase mode
+};
+
+struct DirectPlan {
+  int n_corr;     // series terms used (3, 5 or 8)
+  bool poly_amp;  // (1+u)^(-1/2) by a cubic in u instead of MUFU.RSQ
+  double u_max;
+};
+
+// Chooses the series length and amplitude evaluation for a maximal u;
+// throws ValidationError when the fixed-point mode cannot reach 1e-7 rad.
+DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, double max_dy);
+DirectLayer make_direct_layer(const wcgh_layer& L);
+
+// Launches K3 (and the chunk reduction) on `stream`. pts: device, sorted by
+// layer; layer_begin: host array (n_layers + 1). out: device rows x nh
+// complex64. Returns the number of kernel launches; fills ms via events if
+// `events` (4 events) is non-null.
+struct DirectScratch {
+  DevBuf partial;
+};
+int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
+                  const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
+                  double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
+                  cudaStream_t stream, cudaEvent_t ev_synth_end, double* updates_out);
+
+// ---- analysis (K1 + K2) ----------------------------------------------------
+
+struct AnalysisOut {
+  // device outputs (nullptr = not requested), per layer strided by n^2-type sizes
+  double* pyramid = nullptr;  // layer stride: pyr_len(n)
+  double* sal_pyr = nullptr;  // layer stride: (n/2)^2 + (n/4)^2 + (n/8)^2
+  uint8_t* masks = nullptr;   // layer stride: (n/4)^2 + (n/2)^2 + n^2
+  float* a_eff = nullptr;     // layer stride n^2 (required)
+  float* w_stage = nullptr;   // LUT weights: base (n/8)^2, ll (n/4)^2, l (n/2)^2, full n^2
+  int* seg_counts = nullptr;  // nonzero A_eff per (layer, row, 128-px segment)
+  unsigned long long* ops = nullptr;  // per layer 5 counters (device)
+  int* err = nullptr;                 // validation flags (device)
+};
+
+__host__ __device__ inline size_t pyr_len(int n) {
+  const size_t n2 = size_t(n) * n;
+  return n2 / 64 + 3 * (n2 / 4 + n2 / 16 + n2 / 64);
+}
+__host__ __device__ inline size_t salpyr_len(int n) {
+  const size_t n2 = size_t(n) * n;
+  return n2 / 4 + n2 / 16 + n2 / 64;
+}
+__host__ __device__ inline size_t masks_len(int n) {
+  const size_t n2 = size_t(n) * n;
+  return n2 / 16 + n2 / 4 + n2;
+}
+__host__ __device__ inline size_t wstage_len(int n) {
+  const size_t n2 = size_t(n) * n;
+  return n2 / 64 + n2 / 16 + n2 / 4 + n2;
+}
+__host__ __device__ inline int seg_per_row(int n) { return (n + 127) / 128; }
+
+// Error flag bits written by the analysis kernel.
+enum : int { kErrObjectNonFinite = 1, kErrSaliencyRange = 2 };
+
+int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void* sal,
+                    int sal_dtype, int n, int n_layers, const wcgh_plan& plan,
+                    const AnalysisOut& out, cudaStream_t stream);
+// Exclusive scan of `count` ints into `offsets` (count + 1 entries, last = total).
+int launch_scan(const int* counts, int* offsets, int count, cudaStream_t stream);
+// Ordered compaction of nonzero A_eff into points (hologram coordinates).
+int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers,
+                          int offset, int layer0, wcgh_point* points, cudaStream_t stream);
+// Ordered compaction of nonzero mask bytes into cell indices y*m+x.
+int launch_mask_counts(const uint8_t* mask, int m, int* seg_counts, cudaStream_t stream);
+int launch_compact_mask(const uint8_t* mask, int m, const int* offsets, uint32_t* cells,
+                        cudaStream_t stream);
+
+// Generic L-level Haar analysis (levels != 3); scratch holds 2 n^2 doubles.
+int launch_haar_levels(const void* image, int dtype, double scale, int n, int levels,
+                       double* pyramid, double* scratch, int* err, cudaStream_t stream);
+// refine(): residual expansion + strict gate into dense weights (2m x 2m).
+int launch_refine_gate(const double* h, const double* v, const double* d, int m,
+                       const double* sal, double t, float* w, uint8_t* mask,
+                       unsigned long long* count, cudaStream_t stream);
+// Residual expansion of host-provided bands (wcgh_expand_residual).
+int launch_expand_residual(const double* h, const double* v, const double* d, int m, double* out,
+                           cudaStream_t stream);
+
+// ---- LUT path (K4 + K5) ------------------------------------------------------
+
+// Builds the (2n-1)^2 complex64 support of block size B (fp64 sums).
+int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, DevBuf& scratch,
+                     cudaStream_t stream);
+// plane rows [row0,row0+rows) of an nh-wide plane += superposition of the
+// m x m dense weight grid w (zero = skip) with LUT support of block B;
+// object grid offset `off` (pixels) on the plane.
+int launch_lut_superpose(const float2* lut, int nh, int block, const float* w, int m, int off,
+                         int row0, int rows, float2* plane, cudaStream_t stream, double* updates,
+                         const int* row_nnz);
+int launch_row_nnz(const float* w, int m, int* row_nnz, cudaStream_t stream);
+
+}  // namespace wcgh

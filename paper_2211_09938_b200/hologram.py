@@ -1,0 +1,136 @@
+"""Hologram jobs over the C ABI (wcgh_job_*): resident inputs, device plane.
+
+This is the call a user (or bench.py) makes to synthesize a saliency-gated
+progressive hologram on one GPU; multi-GPU row tiles are in `tiles.py`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+
+@dataclass
+class JobSpec:
+    object_size: int
+    plane_size: int
+    layers: list[tuple[float, float, float]]  # (wavelength, pitch, z) per layer
+    t_ll: float = 0.5
+    t_l: float = 0.7
+    t_full: float = 0.9
+    enable_ll: bool = True
+    enable_l: bool = True
+    enable_full: bool = True
+    method: str = "direct"        # "direct" | "lut"
+    phase: str = "fixed"          # "fixed" | "fp64"
+    row0: int = 0
+    rows: int | None = None
+    obj_dtype: str = "u8"
+    obj_scale: float = 1.0
+    sal_dtype: str = "u8"
+
+
+_DT = {"u8": L.U8, "f32": L.F32, "f64": L.F64}
+_NP = {"u8": np.uint8, "f32": np.float32, "f64": np.float64}
+
+
+class HologramJob:
+    def __init__(self, spec: JobSpec, ctx: L.Context | None = None):
+        self.ctx = ctx or L.default_context()
+        self.spec = spec
+        self.rows = spec.rows if spec.rows is not None else spec.plane_size - spec.row0
+        self._layers = (L.Layer * len(spec.layers))(*[L.Layer(*t) for t in spec.layers])
+        d = L.Desc()
+        d.object_size = spec.object_size
+        d.plane_size = spec.plane_size
+        d.n_layers = len(spec.layers)
+        d.layers = C.cast(self._layers, C.POINTER(L.Layer))
+        d.plan = L.Plan(spec.t_ll, spec.t_l, spec.t_full, int(spec.enable_ll),
+                        int(spec.enable_l), int(spec.enable_full))
+        d.method = L.METHOD_DIRECT if spec.method == "direct" else L.METHOD_LUT
+        if spec.method not in ("direct", "lut"):
+            raise L.ValidationError(f"unknown method {spec.method!r}")
+        d.phase_mode = L.PHASE_FIXED if spec.phase == "fixed" else L.PHASE_FP64
+        d.row0 = spec.row0
+        d.rows = self.rows
+        d.obj_dtype = _DT[spec.obj_dtype]
+        d.obj_scale = spec.obj_scale
+        d.sal_dtype = _DT[spec.sal_dtype]
+        self.desc = d
+        h = C.c_void_p()
+        L.check(self.ctx.lib.wcgh_job_create(self.ctx.h, C.byref(d), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.wcgh_job_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check_inputs(self, objects: np.ndarray, saliency: np.ndarray):
+        n = self.spec.object_size
+        nl = len(self.spec.layers)
+        if objects.size != nl * n * n or saliency.size != nl * n * n:
+            raise L.ValidationError("synthesize_progressive: object/saliency size does not match the scene")
+        if objects.dtype != _NP[self.spec.obj_dtype] or saliency.dtype != _NP[self.spec.sal_dtype]:
+            raise L.ValidationError("object/saliency dtype does not match the job spec")
+
+    def upload(self, objects: np.ndarray, saliency: np.ndarray) -> None:
+        objects = np.ascontiguousarray(objects)
+        saliency = np.ascontiguousarray(saliency)
+        self._check_inputs(objects, saliency)
+        L.check(self.ctx.lib.wcgh_job_upload(self.h, L.ptr(objects), L.ptr(saliency)))
+
+    def upload_dev(self, obj_ptr: int, sal_ptr: int) -> None:
+        L.check(self.ctx.lib.wcgh_job_upload_dev(self.h, C.c_void_p(obj_ptr), C.c_void_p(sal_ptr)))
+
+    def run(self) -> None:
+        L.check(self.ctx.lib.wcgh_job_run(self.h))
+
+    def download(self, out: np.ndarray | None = None) -> np.ndarray:
+        n = self.spec.plane_size
+        if out is None:
+            out = np.empty((self.rows, n), np.complex64)
+        assert out.dtype == np.complex64 and out.flags.c_contiguous and out.size == self.rows * n
+        L.check(self.ctx.lib.wcgh_job_download(self.h, L.ptr(out)))
+        return out
+
+    def download_stages(self) -> np.ndarray:
+        n = self.spec.plane_size
+        out = np.empty((4, self.rows, n), np.complex64)
+        L.check(self.ctx.lib.wcgh_job_download_stages(self.h, L.ptr(out)))
+        return out
+
+    def plane_dev_ptr(self) -> int:
+        return int(self.ctx.lib.wcgh_job_plane_dev(self.h) or 0)
+
+    def stats(self) -> dict:
+        s = L.Stats()
+        L.check(self.ctx.lib.wcgh_job_stats(self.h, C.byref(s)))
+        return {
+            "ops": [int(v) for v in s.ops], "n_points": int(s.n_points), "updates": float(s.updates),
+            "ms_analysis": s.ms_analysis, "ms_synthesis": s.ms_synthesis, "ms_reduce": s.ms_reduce,
+            "ms_total": s.ms_total, "synth_launches": s.synth_launches,
+            "total_launches": s.total_launches,
+        }
+
+    def __call__(self, objects: np.ndarray, saliency: np.ndarray) -> np.ndarray:
+        self.upload(objects, saliency)
+        self.run()
+        return self.download()
+
+
+def spec_for_scene(scene, method: str | None = None, phase: str = "fixed", row0: int = 0,
+                   rows: int | None = None, **plan) -> JobSpec:
+    c = scene.config
+    return JobSpec(object_size=c.object_size, plane_size=c.plane_size,
+                   layers=[(c.wavelength, c.pitch, z) for z in c.depths],
+                   method=method or c.method, phase=phase, row0=row0, rows=rows, **plan)

@@ -1,0 +1,154 @@
+"""numpy-level wrappers of the C-ABI stage entry points (include/wcgh.h).
+
+Each function runs on the GPU through libwcgh.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+
+_DT = {np.dtype(np.uint8): L.U8, np.dtype(np.float32): L.F32, np.dtype(np.float64): L.F64}
+
+
+def _dtype(a: np.ndarray) -> int:
+    try:
+        return _DT[a.dtype]
+    except KeyError:
+        raise L.ValidationError(f"unsupported sample dtype {a.dtype}") from None
+
+
+def _ctx(ctx):
+    return ctx or L.default_context()
+
+
+def haar_analyze(image: np.ndarray, levels: int = 3, scale: float = 1.0, ctx=None) -> np.ndarray:
+    """Flat pyramid: approx, then (h, v, d) per level, finest first."""
+    image = np.ascontiguousarray(image)
+    n = image.shape[0]
+    if image.ndim != 2 or image.shape[1] != n:
+        raise L.ValidationError("haar_analyze: image must be square")
+    t, s = 0, n
+    for _ in range(max(levels, 0)):
+        s //= 2
+        t += 3 * s * s
+    out = np.empty(max(t + s * s, 1))
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_haar_analyze(c.h, L.ptr(image), _dtype(image), scale, n, levels, L.ptr(out)))
+    return out
+
+
+def expand_residual(h, v, d, ctx=None) -> np.ndarray:
+    h, v, d = (np.ascontiguousarray(a, np.float64) for a in (h, v, d))
+    if not (h.shape == v.shape == d.shape):
+        raise L.ValidationError("expand_residual: detail subbands differ in size")
+    m = h.shape[0]
+    out = np.empty((2 * m, 2 * m))
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_expand_residual(c.h, L.ptr(h), L.ptr(v), L.ptr(d), m, L.ptr(out)))
+    return out
+
+
+def quantize_saliency(sal: np.ndarray, ctx=None) -> np.ndarray:
+    sal = np.ascontiguousarray(sal)
+    n = sal.shape[0]
+    if sal.ndim != 2 or sal.shape[1] != n:
+        raise L.ValidationError("quantize_saliency: map must be square")
+    out = np.empty(n * n // 4 + n * n // 16 + n * n // 64)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_quantize_saliency(c.h, L.ptr(sal), _dtype(sal), n, L.ptr(out)))
+    return out
+
+
+def analyze(obj: np.ndarray, sal: np.ndarray, t=(0.5, 0.7, 0.9), en=(1, 1, 1), offset: int = 0,
+            layer: int = 0, obj_scale: float = 1.0, want_points=True, want_cells=True, ctx=None):
+    obj = np.ascontiguousarray(obj)
+    sal = np.ascontiguousarray(sal)
+    n = obj.shape[0]
+    n2 = n * n
+    pyr = np.empty(n2 // 64 + 3 * (n2 // 4 + n2 // 16 + n2 // 64))
+    sp = np.empty(n2 // 4 + n2 // 16 + n2 // 64)
+    masks = np.empty(n2 // 16 + n2 // 4 + n2, np.uint8)
+    a_eff = np.empty((n, n), np.float32)
+    cells = np.empty(n2 // 16 + n2 // 4 + n2, np.uint32) if want_cells else None
+    pts = np.empty(n2, L.POINT_DTYPE) if want_points else None
+    a = L.Analysis()
+    a.pyramid = pyr.ctypes.data_as(C.POINTER(C.c_double))
+    a.sal_pyr = sp.ctypes.data_as(C.POINTER(C.c_double))
+    a.masks = masks.ctypes.data_as(C.POINTER(C.c_uint8))
+    a.a_eff = a_eff.ctypes.data_as(C.POINTER(C.c_float))
+    if cells is not None:
+        a.cells = cells.ctypes.data_as(C.POINTER(C.c_uint32))
+    if pts is not None:
+        a.points = pts.ctypes.data_as(C.POINTER(L.Point))
+    plan = L.Plan(t[0], t[1], t[2], int(en[0]), int(en[1]), int(en[2]))
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_analyze(c.h, L.ptr(obj), _dtype(obj), obj_scale, L.ptr(sal), _dtype(sal), n,
+                               C.byref(plan), offset, layer, C.byref(a)))
+    out = {"pyramid": pyr, "sal_pyr": sp, "masks": masks, "a_eff": a_eff,
+           "ops": np.array(list(a.ops), np.uint64), "n_points": int(a.n_points)}
+    if pts is not None:
+        out["points"] = pts[: a.n_points].copy()
+    if cells is not None:
+        cc = list(a.cell_counts)
+        out["cell_counts"] = cc
+        out["cells"] = [cells[: cc[0]].copy(), cells[cc[0]: cc[0] + cc[1]].copy(),
+                        cells[cc[0] + cc[1]: cc[0] + cc[1] + cc[2]].copy()]
+    return out
+
+
+def synth_points(points: np.ndarray, layers, nh: int, row0: int = 0, rows: int | None = None,
+                 phase: str = "fixed", ctx=None) -> np.ndarray:
+    points = np.ascontiguousarray(points, L.POINT_DTYPE)
+    rows = nh - row0 if rows is None else rows
+    lay = (L.Layer * len(layers))(*[L.Layer(*t) for t in layers])
+    out = np.empty((rows, nh), np.complex64)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_synth_points(c.h, L.ptr(points), len(points), lay, len(layers), nh, row0,
+                                    rows, L.PHASE_FIXED if phase == "fixed" else L.PHASE_FP64,
+                                    L.ptr(out)))
+    return out
+
+
+def build_block_lut(layer, n: int, block: int, ctx=None) -> np.ndarray:
+    span = 2 * n - 1
+    out = np.empty((span, span), np.complex64)
+    lay = L.Layer(*layer)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_build_block_lut(c.h, C.byref(lay), n, block, L.ptr(out)))
+    return out
+
+
+def apply_blocks(plane: np.ndarray, layer, block: int, cells, weights, ctx=None) -> int:
+    """plane (n x n complex64, in place) += sum_i w_i crop(S_B at cell_i)."""
+    assert plane.dtype == np.complex64 and plane.flags.c_contiguous
+    n = plane.shape[0]
+    cells = np.ascontiguousarray(cells, np.uint32)
+    weights = np.ascontiguousarray(weights, np.float32)
+    lay = L.Layer(*layer)
+    ops = C.c_uint64(0)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_apply_blocks(c.h, C.byref(lay), n, block, L.ptr(cells), L.ptr(weights),
+                                    len(cells), L.ptr(plane), C.byref(ops)))
+    return int(ops.value)
+
+
+def refine(plane: np.ndarray, layer, h, v, d, saliency_finer, threshold: float, ctx=None):
+    assert plane.dtype == np.complex64 and plane.flags.c_contiguous
+    n = plane.shape[0]
+    h, v, d = (np.ascontiguousarray(a, np.float64) for a in (h, v, d))
+    sal = np.ascontiguousarray(saliency_finer, np.float64)
+    m = h.shape[0]
+    if v.shape != h.shape or d.shape != h.shape:
+        raise L.ValidationError("refine: residual components differ in size")
+    if sal.shape != (2 * m, 2 * m):
+        raise L.ValidationError("refine: saliency level does not match the residual resolution")
+    mask = np.empty((2 * m, 2 * m), np.uint8)
+    lay = L.Layer(*layer)
+    ops = C.c_uint64(0)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_refine(c.h, C.byref(lay), n, L.ptr(h), L.ptr(v), L.ptr(d), m, L.ptr(sal),
+                              float(threshold), L.ptr(plane), L.ptr(mask), C.byref(ops)))
+    return mask, int(ops.value)
