@@ -115,52 +115,78 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's own code path, bounded sample
 
-def reference_cpu_sample(scene, target_seconds: float = 10.0):
+class ReferenceTimer:
     """Times the UNMODIFIED reference (oracle/_ref) on this workload.
 
     The reference's synthesize_progressive requires object == plane size, so
     the object and mask are zero-padded to the centre of the hologram
-    (SURVEY.md §8(c)). Its cost is linear in the number of nonzero-weight LUT
-    block applications (each one Nh^2 sweep, synthesis.cpp:28-34) plus a
-    per-stage chunk overhead (accumulate_deterministic, parallel.cpp:49-98).
-    We time the reference's multi-threaded refine() (synthesis.cpp:171-178)
+    (SURVEY.md §8(c)); a multi-depth scene is the per-layer sum. Each timed
+    sample is either the reference's whole synthesize_progressive
+    (LutSet::build excluded, like its lut_build precompute) when that fits
+    the per-sample budget, or — for holograms that take minutes to hours on
+    the CPU — an extrapolation: the reference's own multi-threaded refine()
+    (synthesis.cpp:171-178 -> accumulate_deterministic, parallel.cpp:49-98)
     on two contiguous windows of the real gated full-resolution cells
-    (K1 < K2 real operations), fit t(K) = a + b K, and extrapolate to the
-    exact per-stage operation counts of this scene: 4 a + b * ops_nonzero.
-    Falls back to the C restatement (kind "port") when _ref is absent.
+    (K1 < K2 real block applications), fitted as t(K) = a + b K and scaled to
+    this scene's exact nonzero-weight operation count (each operation is one
+    Nh^2 sweep, synthesis.cpp:28-34; zero weights return early, :20).
+    Without _ref the fp64 C restatement is timed instead (kind "port").
     """
-    from oracle import oracle as O
 
-    c = scene.config
-    n, no = c.plane_size, c.object_size
-    off = (n - no) // 2
-    L = c.n_layers
-    xs, ys, amps, lay, ops = O.scene_points(scene.objects.astype(np.float64),
-                                            scene.masks * (1.0 / 255.0), n)
-    points = len(xs)
-    # nonzero-weight operations per stage (zero weights return early in the
-    # reference, synthesis.cpp:20) over all layers
-    nz_ops = 0
-    full_cells = None
-    for l in range(L):
-        obj = scene.objects[l].astype(np.float64)
-        sal = scene.masks[l] * (1.0 / 255.0)
-        an = O.analysis(obj, sal)
-        approx, det = O.split_pyramid(an["pyramid"], no)
-        m_ll, m_l, m_f = np.split(an["masks"], [(no // 4) ** 2, (no // 4) ** 2 + (no // 2) ** 2])
-        r_ll = O.expand_residual(*det[2]).ravel()
-        r_l = O.expand_residual(*det[1]).ravel()
-        r_f = O.expand_residual(*det[0]).ravel()
-        nz_ops += int((approx != 0).sum()) + int(((m_ll != 0) & (r_ll != 0)).sum()) + \
-            int(((m_l != 0) & (r_l != 0)).sum()) + int(((m_f != 0) & (r_f != 0)).sum())
-        if l == 0:
-            full_cells = (det[0], np.flatnonzero((m_f != 0) & (r_f != 0)))
-    if O.ref_available():
-        kind = "reference"
-        workers = O.ref_default_workers()
-        lutset = O.ref().ref_lutset_build(c.wavelength, c.pitch, c.depths[0], n, workers)
-        (h, v, d), cells = full_cells
-        # bands padded into the plane: details[0] lives on the n/2 grid
+    def __init__(self, scene):
+        from oracle import oracle as O
+
+        self.O = O
+        self.scene = scene
+        c = scene.config
+        self.n, self.no = c.plane_size, c.object_size
+        self.off = (self.n - self.no) // 2
+        self.L = c.n_layers
+        xs, ys, amps, lay, ops = O.scene_points(scene.objects.astype(np.float64),
+                                                scene.masks * (1.0 / 255.0), self.n)
+        self.pts = (xs, ys, amps, lay)
+        self.points = len(xs)
+        self.updates = float(self.points) * self.n * self.n
+        nz_ops = 0
+        full_cells = None
+        for l in range(self.L):
+            an = O.analysis(scene.objects[l].astype(np.float64), scene.masks[l] * (1.0 / 255.0))
+            approx, det = O.split_pyramid(an["pyramid"], self.no)
+            no = self.no
+            m_ll, m_l, m_f = np.split(an["masks"], [(no // 4) ** 2, (no // 4) ** 2 + (no // 2) ** 2])
+            r_ll = O.expand_residual(*det[2]).ravel()
+            r_l = O.expand_residual(*det[1]).ravel()
+            r_f = O.expand_residual(*det[0]).ravel()
+            nz_ops += int((approx != 0).sum()) + int(((m_ll != 0) & (r_ll != 0)).sum()) + \
+                int(((m_l != 0) & (r_l != 0)).sum()) + int(((m_f != 0) & (r_f != 0)).sum())
+            if l == 0:
+                full_cells = (det[0], np.flatnonzero((m_f != 0) & (r_f != 0)))
+        self.nz_ops = nz_ops
+        self.full_cells = full_cells
+        self.kind = "reference" if O.ref_available() else "port"
+        self.lutsets = None
+        self.fit = None
+
+    def _luts(self):
+        if self.lutsets is None:
+            c = self.scene.config
+            w = self.O.ref_default_workers()
+            self.workers = w
+            self.lutsets = [self.O.ref().ref_lutset_build(c.wavelength, c.pitch, z, self.n, w)
+                            for z in c.depths]
+        return self.lutsets
+
+    def close(self):
+        if self.lutsets:
+            for h in self.lutsets:
+                self.O.ref().ref_lutset_free(h)
+        self.lutsets = None
+
+    def _refine_window(self, k, rng):
+        import ctypes
+
+        O, n, no, off = self.O, self.n, self.no, self.off
+        (h, v, d), cells = self.full_cells
         hp = np.zeros((n // 2, n // 2))
         vp = np.zeros_like(hp)
         dp = np.zeros_like(hp)
@@ -169,79 +195,130 @@ def reference_cpu_sample(scene, target_seconds: float = 10.0):
         vp[o2:o2 + no // 2, o2:o2 + no // 2] = v
         dp[o2:o2 + no // 2, o2:o2 + no // 2] = d
         cy, cx = np.divmod(cells, no)
-        padded_cells = (cy + off) * n + (cx + off)
+        padded = (cy + off) * n + (cx + off)
+        k = min(k, len(padded))
+        s = int(rng.integers(0, max(1, len(padded) - k)))
+        gate = np.zeros(n * n)
+        gate[padded[s:s + k]] = 1.0
+        secs, opsc = ctypes.c_double(), ctypes.c_uint64()
+        rc = O.ref().ref_time_refine(self._luts()[0], hp.ctypes.data, vp.ctypes.data,
+                                     dp.ctypes.data, n // 2, gate.ctypes.data, 0.5, self.workers,
+                                     ctypes.byref(secs), ctypes.byref(opsc))
+        assert rc == 0, O.ref().ref_last_error()
+        return secs.value, int(opsc.value)
+
+    def estimate(self, budget_s: float):
+        """Extrapolated seconds per hologram from a sample of ~budget_s."""
         rng = np.random.default_rng(1234)
-
-        def run(k):
-            k = min(k, len(padded_cells))
-            s = int(rng.integers(0, max(1, len(padded_cells) - k)))
-            gate = np.zeros(n * n)
-            gate[padded_cells[s:s + k]] = 1.0
-            secs = __import__("ctypes").c_double()
-            opsc = __import__("ctypes").c_uint64()
-            rc = O.ref().ref_time_refine(lutset, hp.ctypes.data, vp.ctypes.data, dp.ctypes.data,
-                                         n // 2, gate.ctypes.data, 0.5, workers,
-                                         __import__("ctypes").byref(secs),
-                                         __import__("ctypes").byref(opsc))
-            assert rc == 0, O.ref().ref_last_error()
-            return secs.value, int(opsc.value)
-
-        # size K2 so the sample is ~target_seconds of CPU work in total
-        t_small, k_small = run(64)
-        per_op = max(t_small / max(k_small, 1), 1e-6)
-        k2 = int(min(len(padded_cells), max(256, 0.6 * target_seconds / per_op)))
+        t0, k0 = self._refine_window(64, rng)
+        per_op = max(t0 / max(k0, 1), 1e-6)
+        k2 = int(max(256, 0.6 * budget_s / per_op))
         k1 = max(64, k2 // 5)
-        t1, o1 = run(k1)
-        t2, o2n = run(k2)
-        b = (t2 - t1) / max(o2n - o1, 1)
+        t1, o1 = self._refine_window(k1, rng)
+        t2, o2 = self._refine_window(k2, rng)
+        b = (t2 - t1) / max(o2 - o1, 1)
         a = max(t1 - b * o1, 0.0)
-        est = 4 * a * L + b * nz_ops
-        O.ref().ref_lutset_free(lutset)
-        sample = (f"reference refine() on {o1}+{o2n} real full-res block applications "
-                  f"(Nh={n}, workers={workers}), t(K)=a+bK fit a={a:.3g}s b={b:.3g}s/op, "
-                  f"extrapolated to {nz_ops} nonzero-weight ops ({L} layer(s), 4 stages)")
-        cores = workers
-    else:
-        kind = "port"
-        cores = 1
+        est = 4 * a * self.L + b * self.nz_ops
+        self.fit = (a, b, o1, o2)
+        return est, (f"reference refine() on {o1}+{o2} real full-res block applications "
+                     f"(Nh={self.n}, workers={self.workers}), t(K)=a+bK fit a={a:.3g}s "
+                     f"b={b:.3g}s/op, extrapolated to {self.nz_ops} nonzero-weight ops "
+                     f"({self.L} layer(s), 4 stages)")
+
+    def full(self):
+        """Seconds for the reference's whole synthesize_progressive (sum over layers)."""
+        import ctypes
+
+        O, n, no, off = self.O, self.n, self.no, self.off
+        total = 0.0
+        for l, h in enumerate(self._luts()):
+            objp = np.zeros((n, n))
+            salp = np.zeros((n, n))
+            objp[off:off + no, off:off + no] = self.scene.objects[l]
+            salp[off:off + no, off:off + no] = self.scene.masks[l] * (1.0 / 255.0)
+            th = np.array([0.5, 0.7, 0.9])
+            en = np.array([1, 1, 1], np.int32)
+            secs = ctypes.c_double()
+            opsr = np.zeros(5, np.uint64)
+            rc = O.ref().ref_time_progressive(h, objp.ctypes.data, salp.ctypes.data,
+                                              th.ctypes.data, en.ctypes.data, self.workers,
+                                              ctypes.byref(secs), None, opsr.ctypes.data)
+            assert rc == 0, O.ref().ref_last_error()
+            total += secs.value
+        return total, (f"reference synthesize_progressive, whole hologram ({self.L} layer(s)): "
+                       f"object zero-padded to the {n}^2 plane, default plan, "
+                       f"workers={self.workers}, LutSet::build excluded (precompute)")
+
+    def port(self):
+        O, c, n = self.O, self.scene.config, self.n
         rng = np.random.default_rng(7)
         npix = 64
         px = rng.integers(0, n, npix)
         py = rng.integers(0, n, npix)
         t0 = time.perf_counter()
-        os.environ.setdefault("OMP_NUM_THREADS", "1")
-        O.direct_pixels(xs, ys, amps, lay, [(c.wavelength, c.pitch, z) for z in c.depths], px, py)
+        O.direct_pixels(*self.pts, [(c.wavelength, c.pitch, z) for z in c.depths], px, py)
         dt = time.perf_counter() - t0
-        est = dt * (n * n) / npix
-        sample = f"oracle direct Eq.(1) fp64 on {npix} pixels x {points} points, extrapolated"
-    updates = float(points) * n * n
-    return {"value": updates / est, "unit": UNIT, "cores": int(cores), "kind": kind,
-            "sample": sample, "ms_per_hologram": est * 1e3, "points": points}
+        return dt * (n * n) / npix, (f"oracle direct Eq.(1) fp64 on {npix} pixels x "
+                                     f"{self.points} points, extrapolated")
+
+    def sample(self, budget_s: float, full_if_below: float | None = None):
+        """One timed sample: (seconds per hologram, description, cores)."""
+        if self.kind == "port":
+            s, d = self.port()
+            return s, d, os.cpu_count() or 1
+        if getattr(self, "use_full", None) is None:
+            est, desc = self.estimate(min(budget_s, 10.0))
+            limit = budget_s if full_if_below is None else full_if_below
+            self.use_full = est <= limit
+            if not self.use_full:
+                return est, desc, self.workers
+        if self.use_full:
+            s, d = self.full()
+            return s, d, self.workers
+        est, desc = self.estimate(min(budget_s, 10.0))
+        return est, desc, self.workers
+
+
+def reference_cpu_sample(scene, target_seconds: float = 10.0):
+    t = ReferenceTimer(scene)
+    try:
+        secs, desc, cores = t.sample(target_seconds, full_if_below=3 * target_seconds)
+    finally:
+        t.close()
+    return {"value": t.updates / secs, "unit": UNIT, "cores": int(cores), "kind": t.kind,
+            "sample": desc, "ms_per_hologram": secs * 1e3, "points": t.points}
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation on the box's
+    host cores (rank 0 only), same metric/config as our arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from paper_2211_09938_b200 import scenes
 
     sc = scenes.make_scene(args.config)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = reference_cpu_sample(sc, target_seconds=max(1.0, args.cpu_seconds / 3))
-        if i >= args.warmup:
-            vals.append(r)
-    v = float(np.median([r["value"] for r in vals]))
-    ms = float(np.median([r["ms_per_hologram"] for r in vals]))
-    last = vals[-1]
+    t = ReferenceTimer(sc)
+    per_step = max(2.0, 150.0 / max(1, args.steps + min(args.warmup, 1)))
+    secs = []
+    try:
+        for i in range(min(args.warmup, 1) + args.steps):
+            s, desc, cores = t.sample(per_step)
+            if i >= min(args.warmup, 1):
+                secs.append(s)
+    finally:
+        t.close()
+    ms = float(np.mean(secs)) * 1e3
+    v = t.updates / (ms * 1e-3)
     out = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": sc.config.name, "object": sc.config.object_size,
-                   "plane": sc.config.plane_size, "points": last["points"], "method": "lut (reference)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
-                         "sample": last["sample"]},
+                   "plane": sc.config.plane_size, "points": t.points,
+                   "method": "reference LUT synthesize_progressive (CPU)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(cores), "kind": t.kind,
+                         "sample": desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))

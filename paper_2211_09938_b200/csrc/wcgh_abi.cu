@@ -68,6 +68,7 @@ struct wcgh_job {
   DevBuf w_stage, row_nnz, stage_planes, lut_scratch;
   std::vector<std::unique_ptr<DevBuf>> luts;  // [layer * 4 + stage]
   DirectScratch direct;
+  DirectTiming timing;
   // pinned host staging
   int64_t* h_offsets = nullptr;       // n_layers + 1
   unsigned long long* h_ops = nullptr;  // n_layers * 5
@@ -644,6 +645,7 @@ void finish_stats(wcgh_job* j, const unsigned long long* ops) {
 void run_job_direct(wcgh_job* j, cudaStream_t s) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
+  j->timing.reset();
   WCGH_CUDA(cudaEventRecord(j->ev[0], s));
   run_analysis(j, s, false);
   const size_t per_layer = size_t(No) * seg_per_row(No);
@@ -674,14 +676,16 @@ void run_job_direct(wcgh_job* j, cudaStream_t s) {
                                  std::fabs(double(d.row0 + d.rows - 1) - j->off));
   const int launches = launch_direct(j->points.as<wcgh_point>(), lb, L, d.layers, d.plane_size,
                                      d.row0, d.rows, d.phase_mode, far, max_dy,
-                                     j->plane.as<float2>(), j->direct, s, j->ev[2], &j->stats.updates);
-  j->stats.synth_launches = 1;
+                                     j->plane.as<float2>(), j->direct, s, &j->timing, &j->stats.updates);
+  j->stats.synth_launches = j->timing.launches();
   j->stats.total_launches += launches;
   WCGH_CUDA(cudaEventRecord(j->ev[3], s));
   sync(s);
   WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_analysis, j->ev[0], j->ev[1]));
-  WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_synthesis, j->ev[1], j->ev[2]));
-  WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_reduce, j->ev[2], j->ev[3]));
+  j->stats.ms_synthesis = j->timing.elapsed_ms();
+  float synth_phase = 0.f;
+  WCGH_CUDA(cudaEventElapsedTime(&synth_phase, j->ev[1], j->ev[3]));
+  j->stats.ms_reduce = std::max(0.f, synth_phase - j->stats.ms_synthesis);
   WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_total, j->ev[0], j->ev[3]));
 }
 

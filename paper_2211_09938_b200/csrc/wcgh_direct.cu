@@ -8,17 +8,20 @@
 // l of warp w owns pixels (x_b + l + 32 i, y_0 + w), i < P, and keeps their
 // complex sums in registers. Points stream through shared memory in batches
 // of 256 16-byte records and are broadcast to all threads. The point list is
-// split into chunks whose boundaries depend only on the point count, each
-// chunk producing a partial plane that a fixed-order reduction sums: the
-// per-pixel summation order is independent of the launch and of the row-band
+// cut into fixed chunks of kChunk points (boundaries depend on nothing but
+// the point index); each (tile, chunk) CTA writes its chunk's partial sum and
+// a reduction adds the partials in chunk order. The per-pixel summation
+// order is therefore independent of the launch shape and of the row-band
 // split across GPUs (the GPU analogue of accumulate_deterministic,
-// parallel.cpp:49-98), so results are bitwise identical for any GPU count.
+// parallel.cpp:49-98): holograms are bitwise identical for any GPU count.
+// Chunks also bound the fp32 accumulation length (1024 terms per partial).
 //
 // Phase (fixed mode): cycles = frac(z/lambda) + s*alpha + (z/lambda) g(u), with
 // the quadratic term in exact 0.64/0.32 fixed point and advanced along a
 // thread's pixels by an exact second-order recurrence (two IADDs), and the
 // small higher-order term g(u) = sqrt(1+u)-1-u/2 as an fp32 series. fp32
 // k*r would lose the phase entirely (k r ~ 2.4e6 rad); see SURVEY.md App. A.
+// Per update: 2 MUFU (sin, cos) + ~14 FMA/ALU-pipe instructions.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,6 +37,8 @@ namespace {
 
 constexpr int kBatch = 256;
 constexpr int kThreads = 256;
+constexpr long long kChunk = 1024;          // points per partial sum
+constexpr size_t kPartialBytes = 2ull << 30;  // partial-plane budget per launch group
 constexpr float kTwoPi = 6.283185307179586f;
 constexpr float kNegThreePi = -9.42477796076938f;
 
@@ -42,10 +47,19 @@ __device__ __forceinline__ float i2f_small(int v) {
   return __int_as_float(v + 0x4B400000) - 12582912.0f;
 }
 
-template <int P, int NC, bool POLY_AMP>
-__global__ void __launch_bounds__(kThreads, 2)
+// Chunk c of the point list, restricted to layer l: [s0, s1).
+__device__ __forceinline__ void layer_span(const long long* lb, int l, long long p0, long long p1,
+                                           long long& s0, long long& s1) {
+  s0 = max(p0, lb[l]);
+  s1 = min(p1, lb[l + 1]);
+}
+
+// NC: phase-series terms (b_2 .. b_{NC+1}); AMP: 0 = MUFU.RSQ, 2/3 = degree of
+// the (1+u)^(-1/2) polynomial.
+template <int P, int NC, int AMP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_direct_fixed(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
-                   int n_layers, long long chunk, long long n_points, int nh, int row0, int rows,
+                   int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                    int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
   const int lane = threadIdx.x & 31;
@@ -55,16 +69,16 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int row = ty * 8 + warp;  // row within the band
   const int y = row0 + row;       // hologram row
   const int xb = tx * 32 * P + lane;
-  const long long p0 = (long long)blockIdx.y * chunk;
-  const long long p1 = min(p0 + chunk, n_points);
+  const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
+  const long long p1 = min(p0 + kChunk, n_points);
 
-  float tre[P], tim[P];
+  float re[P], im[P];
 #pragma unroll
-  for (int i = 0; i < P; ++i) tre[i] = tim[i] = 0.0f;
+  for (int i = 0; i < P; ++i) re[i] = im[i] = 0.0f;
 
   for (int l = 0; l < n_layers; ++l) {
-    const long long s0 = max(p0, layer_begin[l]);
-    const long long s1 = min(p1, layer_begin[l + 1]);
+    long long s0, s1;
+    layer_span(layer_begin, l, p0, p1, s0, s1);
     if (s0 >= s1) continue;
     const DirectLayer& L = c_layers[l];
     const uint32_t a_hi = L.a_hi, a_lo = L.a_lo, phi0 = L.phi0, dd = L.dd;
@@ -80,10 +94,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncthreads();
       if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
       __syncthreads();
-
-      float re[P], im[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) re[i] = im[i] = 0.0f;
 
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
@@ -108,11 +118,13 @@ __global__ void __launch_bounds__(kThreads, 2)
           float pc = corr[NC - 1];
 #pragma unroll
           for (int k = NC - 2; k >= 0; --k) pc = fmaf(pc, u, corr[k]);
-          // radians in [-pi, pi) + correction: (phf - 1.5) * 2pi + u^2 * pc
+          // radians: (phf - 1.5) * 2pi + u^2 * pc (phi0 carries the half cycle)
           const float ph = fmaf(phf, kTwoPi, fmaf(u2, pc, kNegThreePi));
           float am;
-          if constexpr (POLY_AMP) {
+          if constexpr (AMP == 3) {
             am = fmaf(fmaf(fmaf(a3, u, a2), u, a1), u, a0);
+          } else if constexpr (AMP == 2) {
+            am = fmaf(fmaf(a2, u, a1), u, a0);
           } else {
             am = a0 * rsqrtf(1.0f + u);
           }
@@ -126,11 +138,6 @@ __global__ void __launch_bounds__(kThreads, 2)
           du += ddu;
         }
       }
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        tre[i] += re[i];
-        tim[i] += im[i];
-      }
     }
   }
 
@@ -139,17 +146,17 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int x = xb + 32 * i;
-      if (x < nh) dst[x] = make_float2(tre[i], tim[i]);
+      if (x < nh) dst[x] = make_float2(re[i], im[i]);
     }
   }
 }
 
 // Double-phase option: r and k*r in fp64, reduced to [-pi, pi] in fp64, then
-// fp32 sin/cos. Accuracy mode (FP64 pipe bound).
+// fp32 sin/cos. Accuracy mode (FP64-pipe bound).
 template <int P>
 __global__ void __launch_bounds__(kThreads)
     k_direct_fp64(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
-                  int n_layers, long long chunk, long long n_points, int nh, int row0, int rows,
+                  int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                   int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
   const int lane = threadIdx.x & 31;
@@ -159,17 +166,17 @@ __global__ void __launch_bounds__(kThreads)
   const int row = ty * 8 + warp;
   const int y = row0 + row;
   const int xb = tx * 32 * P + lane;
-  const long long p0 = (long long)blockIdx.y * chunk;
-  const long long p1 = min(p0 + chunk, n_points);
+  const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
+  const long long p1 = min(p0 + kChunk, n_points);
   const double two_pi = 6.283185307179586476925286766559;
 
-  float tre[P], tim[P];
+  float re[P], im[P];
 #pragma unroll
-  for (int i = 0; i < P; ++i) tre[i] = tim[i] = 0.0f;
+  for (int i = 0; i < P; ++i) re[i] = im[i] = 0.0f;
 
   for (int l = 0; l < n_layers; ++l) {
-    const long long s0 = max(p0, layer_begin[l]);
-    const long long s1 = min(p1, layer_begin[l + 1]);
+    long long s0, s1;
+    layer_span(layer_begin, l, p0, p1, s0, s1);
     if (s0 >= s1) continue;
     const double pitch = c_layers[l].pitch, z = c_layers[l].z, k = c_layers[l].k;
     const double z2 = z * z;
@@ -178,9 +185,6 @@ __global__ void __launch_bounds__(kThreads)
       __syncthreads();
       if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
       __syncthreads();
-      float re[P], im[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) re[i] = im[i] = 0.0f;
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
         const int4 q = sp[j];
@@ -199,11 +203,6 @@ __global__ void __launch_bounds__(kThreads)
           im[i] = fmaf(am, sn, im[i]);
         }
       }
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        tre[i] += re[i];
-        tim[i] += im[i];
-      }
     }
   }
   if (row < rows) {
@@ -211,17 +210,23 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int x = xb + 32 * i;
-      if (x < nh) dst[x] = make_float2(tre[i], tim[i]);
+      if (x < nh) dst[x] = make_float2(re[i], im[i]);
     }
   }
 }
 
-// Fixed-order chunk reduction in fp64: out = sum_c partial[c].
+// Fixed-order chunk reduction: out (+)= sum_c partial[c], c in chunk order,
+// accumulated in fp64.
 __global__ void k_reduce_chunks(const float2* __restrict__ partial, int n_chunks, size_t count,
-                                float2* __restrict__ out) {
+                                int accumulate, float2* __restrict__ out) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double re = 0.0, im = 0.0;
+  if (accumulate) {
+    const float2 o = out[i];
+    re = o.x;
+    im = o.y;
+  }
   for (int c = 0; c < n_chunks; ++c) {
     const float2 v = partial[size_t(c) * count + i];
     re += v.x;
@@ -237,29 +242,48 @@ double binom(double a, int n) {
   return r;
 }
 
-template <int P, int NC, bool POLY>
-void launch_fixed(dim3 grid, cudaStream_t s, const int4* pts, const long long* lb, int L,
-                  long long chunk, long long np, int nh, int row0, int rows, int tiles_x,
-                  float2* out, size_t stride) {
-  k_direct_fixed<P, NC, POLY><<<grid, kThreads, 0, s>>>(pts, lb, L, chunk, np, nh, row0, rows,
-                                                        tiles_x, out, stride);
+struct LaunchArgs {
+  dim3 grid;
+  cudaStream_t s;
+  const int4* pts;
+  const long long* lb;
+  int L;
+  long long np;
+  int chunk0, nh, row0, rows, tiles_x;
+  float2* out;
+  size_t stride;
+};
+
+template <int P, int NC, int AMP>
+void launch_fixed(const LaunchArgs& a) {
+  constexpr int MINB = 2;
+  k_direct_fixed<P, NC, AMP, MINB><<<a.grid, kThreads, 0, a.s>>>(
+      a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+}
+
+template <int P, int NC>
+void launch_fixed_amp(const DirectPlan& plan, const LaunchArgs& a) {
+  if (plan.amp_degree == 2)
+    launch_fixed<P, NC, 2>(a);
+  else if (plan.amp_degree == 3)
+    launch_fixed<P, NC, 3>(a);
+  else
+    launch_fixed<P, NC, 0>(a);
 }
 
 template <int P>
-void launch_fixed_nc(const DirectPlan& plan, dim3 grid, cudaStream_t s, const int4* pts,
-                     const long long* lb, int L, long long chunk, long long np, int nh, int row0,
-                     int rows, int tiles_x, float2* out, size_t stride) {
-#define WCGH_LF(NC, POLY) \
-  launch_fixed<P, NC, POLY>(grid, s, pts, lb, L, chunk, np, nh, row0, rows, tiles_x, out, stride)
-  if (plan.n_corr <= 3) {
-    if (plan.poly_amp) WCGH_LF(3, true); else WCGH_LF(3, false);
-  } else if (plan.n_corr <= 5) {
-    if (plan.poly_amp) WCGH_LF(5, true); else WCGH_LF(5, false);
-  } else {
-    if (plan.poly_amp) WCGH_LF(8, true); else WCGH_LF(8, false);
-  }
-#undef WCGH_LF
+void launch_fixed_nc(const DirectPlan& plan, const LaunchArgs& a) {
+  if (plan.n_corr <= 2)
+    launch_fixed_amp<P, 2>(plan, a);
+  else if (plan.n_corr <= 3)
+    launch_fixed_amp<P, 3>(plan, a);
+  else if (plan.n_corr <= 5)
+    launch_fixed_amp<P, 5>(plan, a);
+  else
+    launch_fixed_amp<P, 8>(plan, a);
 }
+
+int pixels_per_thread(int nh) { return nh >= 1024 ? 32 : (nh >= 512 ? 16 : 4); }
 
 }  // namespace
 
@@ -273,7 +297,10 @@ DirectLayer make_direct_layer(const wcgh_layer& L) {
   d.a_hi = uint32_t(hi);
   d.a_lo = uint32_t(lo);
   const double K = z / lam;
-  d.phi0 = uint32_t(uint64_t(std::llround(std::ldexp(K - std::floor(K), 32))) & 0xffffffffu);
+  // + half a cycle: the kernel reads the phase as (1 + frac(t)) - 1.5 cycles,
+  // i.e. centred in [-1/2, 1/2), so t carries frac(z/lambda) + 1/2.
+  const double K2 = K + 0.5;
+  d.phi0 = uint32_t(uint64_t(std::llround(std::ldexp(K2 - std::floor(K2), 32))) & 0xffffffffu);
   const double ddc = 2048.0 * alpha;
   d.dd = uint32_t(uint64_t(std::llround(std::ldexp(ddc - std::floor(ddc), 32))) & 0xffffffffu);
   d.c = float(p * p / (z * z));
@@ -288,12 +315,16 @@ DirectLayer make_direct_layer(const wcgh_layer& L) {
   return d;
 }
 
+// Series lengths for the fixed-point mode. Budgets: phase truncation <= 4e-6
+// rad and amplitude truncation <= 2e-6 relative — systematic errors 25-50x
+// below the 1e-4 relative-L2 bar (BASELINE.json north_star).
 DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, double max_dy) {
-  DirectPlan plan{3, true, 0.0};
+  constexpr double kPhaseTol = 4e-6, kAmpTol = 2e-6;
+  DirectPlan plan{2, 2, 0.0};
   const double two_pi = 6.283185307179586476925286766559;
   const double s_max = max_dx * max_dx + max_dy * max_dy;
-  int need = 3;
-  bool poly = true;
+  int need = 2;
+  bool amp3 = false, amp_rsqrt = false;
   for (int l = 0; l < n_layers; ++l) {
     const double p = layers[l].pitch, z = layers[l].z, K = layers[l].z / layers[l].wavelength;
     const double u = s_max * p * p / (z * z);
@@ -302,98 +333,91 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
                      "(u_max >= 0.5); use WCGH_PHASE_FP64");
     int nc = 0;
     for (nc = 1; nc <= kMaxCorr; ++nc) {
-      // truncation after b_2..b_{nc+1}: next term bounds the tail for u < 1/2
+      // truncation after b_2..b_{nc+1}: the next term bounds the tail for u < 1/2
       const double tail = two_pi * K * std::fabs(binom(0.5, nc + 2)) * std::pow(u, nc + 2) / (1.0 - u);
-      if (tail <= 1e-7) break;
+      if (tail <= kPhaseTol) break;
     }
     require(nc <= kMaxCorr, "direct (fixed phase): correction series does not converge to "
-                            "1e-7 rad; use WCGH_PHASE_FP64");
+                            "4e-6 rad; use WCGH_PHASE_FP64");
     need = std::max(need, nc);
-    // cubic (1+u)^(-1/2): relative tail below 2e-8
-    if (std::fabs(binom(-0.5, 4)) * std::pow(u, 4) / (1.0 - u) > 2e-8) poly = false;
+    const auto amp_tail = [&](int deg) {
+      return std::fabs(binom(-0.5, deg + 1)) * std::pow(u, deg + 1) / (1.0 - u);
+    };
+    if (amp_tail(2) > kAmpTol) {
+      if (amp_tail(3) <= kAmpTol)
+        amp3 = true;
+      else
+        amp_rsqrt = true;
+    }
   }
-  plan.n_corr = need <= 3 ? 3 : (need <= 5 ? 5 : 8);
-  plan.poly_amp = poly;
+  plan.n_corr = need <= 2 ? 2 : (need <= 3 ? 3 : (need <= 5 ? 5 : 8));
+  plan.amp_degree = amp_rsqrt ? 0 : (amp3 ? 3 : 2);
   return plan;
 }
 
 int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
-                  cudaStream_t stream, cudaEvent_t ev_synth_end, double* updates_out) {
+                  cudaStream_t stream, DirectTiming* timing, double* updates_out) {
   require(n_layers >= 1 && n_layers <= kMaxLayers, "direct: 1..16 layers");
   require(rows >= 1 && row0 >= 0 && row0 + rows <= nh, "direct: row band outside the plane");
+  require(phase_mode == WCGH_PHASE_FIXED || phase_mode == WCGH_PHASE_FP64,
+          "direct: unknown phase mode");
   const long long n_points = layer_begin_host[n_layers];
   if (updates_out) *updates_out = double(n_points) * double(rows) * double(nh);
-  int launches = 0;
+  const size_t band = size_t(rows) * nh;
   if (n_points == 0) {
-    WCGH_CUDA(cudaMemsetAsync(out_dev, 0, size_t(rows) * nh * sizeof(float2), stream));
-    if (ev_synth_end) WCGH_CUDA(cudaEventRecord(ev_synth_end, stream));
+    WCGH_CUDA(cudaMemsetAsync(out_dev, 0, band * sizeof(float2), stream));
     return 0;
   }
+  DirectPlan plan{};
+  if (phase_mode == WCGH_PHASE_FIXED) plan = plan_direct(layers, n_layers, max_dx, max_dy);
   DirectLayer h_layers[kMaxLayers];
   for (int l = 0; l < n_layers; ++l) h_layers[l] = make_direct_layer(layers[l]);
   WCGH_CUDA(cudaMemcpyToSymbolAsync(c_layers, h_layers, sizeof(DirectLayer) * n_layers, 0,
                                     cudaMemcpyHostToDevice, stream));
-  // layer offsets live in a small device array appended to the scratch
-  // Chunking depends on the point count only (determinism across row splits).
-  const long long target = 64;
-  long long chunk = (n_points + target - 1) / target;
-  chunk = std::max<long long>(kBatch, ((chunk + kBatch - 1) / kBatch) * kBatch);
-  const int n_chunks = int((n_points + chunk - 1) / chunk);
 
-  const int P = nh >= 512 ? 16 : (nh >= 256 ? 8 : 4);
+  const int n_chunks = int((n_points + kChunk - 1) / kChunk);
+  const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
+  const int P = pixels_per_thread(nh);
   const int tiles_x = (nh + 32 * P - 1) / (32 * P);
   const int tiles_y = (rows + 7) / 8;
-  const size_t band = size_t(rows) * nh;
-  const size_t stride = size_t(tiles_y) * 8 * nh;  // partial planes cover whole tiles
   const size_t lb_bytes = sizeof(long long) * (n_layers + 1);
-  const size_t part_bytes = n_chunks > 1 ? stride * n_chunks * sizeof(float2) : 0;
-  char* base = static_cast<char*>(scratch.partial.reserve(part_bytes + 256 + lb_bytes));
-  long long* lb_dev = reinterpret_cast<long long*>(base + part_bytes + 256 - (part_bytes % 256));
+  const size_t part_bytes = ((band * group * sizeof(float2)) + 255) / 256 * 256;
+  char* base = static_cast<char*>(scratch.partial.reserve(part_bytes + lb_bytes));
+  long long* lb_dev = reinterpret_cast<long long*>(base + part_bytes);
+  float2* partial = reinterpret_cast<float2*>(base);
   static_assert(sizeof(long long) == sizeof(int64_t), "int64");
   WCGH_CUDA(cudaMemcpyAsync(lb_dev, layer_begin_host, lb_bytes, cudaMemcpyHostToDevice, stream));
 
-  float2* target_plane = n_chunks > 1 ? reinterpret_cast<float2*>(base) : out_dev;
-  const size_t out_stride = n_chunks > 1 ? stride : 0;
-  // With one chunk the kernel writes the band directly; rows beyond `rows`
-  // are masked by the kernel (row < rows).
-  dim3 grid(unsigned(tiles_x * tiles_y), unsigned(n_chunks));
-  const int4* p4 = reinterpret_cast<const int4*>(pts_dev);
-  if (phase_mode == WCGH_PHASE_FP64) {
-    if (P == 16)
-      k_direct_fp64<16><<<grid, kThreads, 0, stream>>>(p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-    else if (P == 8)
-      k_direct_fp64<8><<<grid, kThreads, 0, stream>>>(p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-    else
-      k_direct_fp64<4><<<grid, kThreads, 0, stream>>>(p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-  } else {
-    require(phase_mode == WCGH_PHASE_FIXED, "direct: unknown phase mode");
-    const DirectPlan plan = plan_direct(layers, n_layers, max_dx, max_dy);
-    if (P == 16)
-      launch_fixed_nc<16>(plan, grid, stream, p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-    else if (P == 8)
-      launch_fixed_nc<8>(plan, grid, stream, p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-    else
-      launch_fixed_nc<4>(plan, grid, stream, p4, lb_dev, n_layers, chunk, n_points, nh, row0, rows, tiles_x, target_plane, out_stride);
-  }
-  WCGH_CHECK_LAUNCH();
-  ++launches;
-  if (ev_synth_end) WCGH_CUDA(cudaEventRecord(ev_synth_end, stream));
-  if (n_chunks > 1) {
-    // partial planes are laid out with a tile-rounded row count; reduce the band
-    // row by row region: stride == band when rows % 8 == 0.
-    if (stride == band) {
-      k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(target_plane, n_chunks, band, out_dev);
-      WCGH_CHECK_LAUNCH();
-      ++launches;
+  int launches = 0;
+  for (int g0 = 0; g0 < n_chunks; g0 += group) {
+    const int ng = std::min(group, n_chunks - g0);
+    LaunchArgs a{dim3(unsigned(tiles_x * tiles_y), unsigned(ng)), stream,
+                 reinterpret_cast<const int4*>(pts_dev), lb_dev, n_layers, n_points, g0, nh,
+                 row0, rows, tiles_x, partial, band};
+    if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), stream));
+    if (phase_mode == WCGH_PHASE_FP64) {
+      if (P == 32)
+        k_direct_fp64<32><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+      else if (P == 16)
+        k_direct_fp64<16><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+      else
+        k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
     } else {
-      // rows not a multiple of 8: reduce the padded layout, then the band is its prefix
-      k_reduce_chunks<<<unsigned((stride + 255) / 256), 256, 0, stream>>>(target_plane, n_chunks, stride, target_plane);
-      WCGH_CHECK_LAUNCH();
-      WCGH_CUDA(cudaMemcpyAsync(out_dev, target_plane, band * sizeof(float2), cudaMemcpyDeviceToDevice, stream));
-      ++launches;
+      if (P == 32)
+        launch_fixed_nc<32>(plan, a);
+      else if (P == 16)
+        launch_fixed_nc<16>(plan, a);
+      else
+        launch_fixed_nc<4>(plan, a);
     }
+    WCGH_CHECK_LAUNCH();
+    if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), stream));
+    k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(partial, ng, band, g0 > 0,
+                                                                      out_dev);
+    WCGH_CHECK_LAUNCH();
+    launches += 2;
   }
   return launches;
 }

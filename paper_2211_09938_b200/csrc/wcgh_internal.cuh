@@ -85,9 +85,41 @@ struct DirectLayer {
 };
 
 struct DirectPlan {
-  int n_corr;     // series terms used (3, 5 or 8)
-  bool poly_amp;  // (1+u)^(-1/2) by a cubic in u instead of MUFU.RSQ
+  int n_corr;      // phase-series terms used (2, 3, 5 or 8)
+  int amp_degree;  // (1+u)^(-1/2): polynomial degree 2 or 3, or 0 = MUFU.RSQ
   double u_max;
+};
+
+// CUDA-event pairs around each launch of a kernel family (for per-kernel
+// device time inside a run); events are created lazily and reused.
+struct DirectTiming {
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      WCGH_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+  cudaEvent_t begin() { return next(); }
+  cudaEvent_t end() { return next(); }
+  void reset() { used = 0; }
+  // Sum of the pair durations (call after the stream has synchronized).
+  float elapsed_ms() const {
+    float total = 0.f;
+    for (size_t i = 0; i + 1 < used; i += 2) {
+      float ms = 0.f;
+      WCGH_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      total += ms;
+    }
+    return total;
+  }
+  int launches() const { return int(used / 2); }
+  ~DirectTiming() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
 };
 
 // Chooses the series length and amplitude evaluation for a maximal u;
@@ -95,17 +127,17 @@ struct DirectPlan {
 DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, double max_dy);
 DirectLayer make_direct_layer(const wcgh_layer& L);
 
-// Launches K3 (and the chunk reduction) on `stream`. pts: device, sorted by
+// Launches K3 (and the chunk reductions) on `stream`. pts: device, sorted by
 // layer; layer_begin: host array (n_layers + 1). out: device rows x nh
-// complex64. Returns the number of kernel launches; fills ms via events if
-// `events` (4 events) is non-null.
+// complex64. Returns the number of kernel launches; if `timing` is given,
+// brackets every K3 launch with an event pair.
 struct DirectScratch {
   DevBuf partial;
 };
 int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
-                  cudaStream_t stream, cudaEvent_t ev_synth_end, double* updates_out);
+                  cudaStream_t stream, DirectTiming* timing, double* updates_out);
 
 // ---- analysis (K1 + K2) ----------------------------------------------------
 
