@@ -162,6 +162,9 @@ class ReferenceTimer:
             if l == 0:
                 full_cells = (det[0], np.flatnonzero((m_f != 0) & (r_f != 0)))
         self.nz_ops = nz_ops
+        if c.method == "lut":
+            # LUT configs count (nonzero gated cell, pixel) updates on both arms
+            self.updates = float(nz_ops) * self.n * self.n
         self.full_cells = full_cells
         self.kind = "reference" if O.ref_available() else "port"
         self.lutsets = None
@@ -440,23 +443,32 @@ def main():
     if rank == 0:
         peaks = measured_peaks()
         f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        peak = SM_COUNT * f_max * MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE
-        # dominant kernel: the accumulation (K3), timed by CUDA events around its
-        # launch on this stream inside wcgh_job_run; per-rank updates per launch
+        f_meas = (clk.get("sm_mhz") or 0) * 1e6
+        # dominant kernel, timed by CUDA events around its launches on this
+        # stream inside wcgh_job_run; per-rank algorithmic updates per step
         k_ms = float(np.mean(synth_ms))
         rank_updates = float(points) * rows * c.plane_size
         achieved = rank_updates / (k_ms * 1e-3)
-        f_meas = (clk.get("sm_mhz") or 0) * 1e6
+        if job.spec.method == "direct":
+            per_clk, kernel = MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE, "k_direct_fixed (K3)"
+            basis = (f"canonical SFU roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz (MEASURED_PEAKS "
+                     "sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)); the kernel "
+                     "issues 2 MUFU + ~15 FMA/ALU per update; not an HBM or tensor-core kernel")
+            bound = "sfu"
+            dram = int(points * 16 + rows * c.plane_size * 8)
+        else:
+            per_clk, kernel = 128.0 / 2.0, "k_lut_superpose (K4), 4 stage launches"
+            basis = (f"FP32 roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz x 128 FFMA/clk/SM / 2 FFMA per "
+                     "(nonzero cell, pixel) update (SURVEY.md §8(d))")
+            bound = "fp32"
+            dram = int(4 * (2 * c.plane_size - 1) ** 2 * 8 + rows * c.plane_size * 8)
+        peak = SM_COUNT * f_max * per_clk
         roof = {
-            "bound": "sfu", "achieved": achieved, "peak": peak, "unit": UNIT,
-            "frac": achieved / peak, "traffic": None,
-            "kernel": "k_direct_fixed (K3)", "kernel_ms": k_ms,
-            "peak_basis": (f"canonical SFU roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz (MEASURED_PEAKS "
-                           f"sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)); "
-                           "not an HBM or tensor-core kernel"),
-            "frac_at_measured_clock": (achieved / (SM_COUNT * f_meas * MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE)
-                                       if f_meas else None),
-            "dram_bytes_per_launch_algorithmic": int(points * 16 + rows * c.plane_size * 8),
+            "bound": bound, "achieved": achieved, "peak": peak, "unit": UNIT,
+            "frac": achieved / peak, "traffic": None, "kernel": kernel, "kernel_ms": k_ms,
+            "peak_basis": basis,
+            "frac_at_measured_clock": (achieved / (SM_COUNT * f_meas * per_clk) if f_meas else None),
+            "dram_bytes_per_step_algorithmic": dram,
         }
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -101,7 +101,8 @@ typedef struct {
 /* Statistics of the last wcgh_job_run. */
 typedef struct {
   uint64_t ops[WCGH_OP_LEVELS]; /* summed over layers */
-  int64_t n_points;             /* compacted nonzero A_eff points (direct) */
+  int64_t n_points;             /* direct: compacted nonzero A_eff points;
+                                   LUT: nonzero-weight gated cells, all stages */
   double updates;               /* algorithmic updates of the synthesis kernel */
   float ms_analysis;            /* device time: DWT + gate + compaction */
   float ms_synthesis;           /* device time: accumulation kernel(s) */

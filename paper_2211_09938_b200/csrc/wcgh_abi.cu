@@ -52,8 +52,9 @@ struct wcgh_ctx {
   int sm_count = 0;
   std::string name;
   // scratch for the stage entry points
-  DevBuf b_in, b_in2, b_out, b_out2, b_misc, b_pts, b_plane, b_lut, b_lut_scratch;
+  DevBuf b_in, b_in2, b_out, b_out2, b_misc, b_pts, b_plane, b_lut, b_lut_scratch, lut_partial;
   DirectScratch direct;
+  StageCells cells;
   std::mutex mu;
 };
 
@@ -65,8 +66,10 @@ struct wcgh_job {
   size_t in_elems = 0;  // per layer No^2
   DevBuf obj, sal, a_eff, seg_counts, seg_offsets, ops, err, points, plane;
   // LUT method
-  DevBuf w_stage, row_nnz, stage_planes, lut_scratch;
-  std::vector<std::unique_ptr<DevBuf>> luts;  // [layer * 4 + stage]
+  DevBuf w_stage, stage_planes, lut_scratch, lut_partial;
+  StageCells cells[4];
+  std::vector<std::unique_ptr<DevBuf>> luts;  // [layer * 4 + stage], guarded allocations
+  std::vector<float2*> lut_base;              // support element (0, 0) in each
   DirectScratch direct;
   DirectTiming timing;
   // pinned host staging
@@ -431,7 +434,7 @@ int wcgh_build_block_lut(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int bloc
     use_device(ctx);
     cudaStream_t s = ctx->stream;
     const size_t span = size_t(2 * n - 1);
-    float2* lut = static_cast<float2*>(ctx->b_lut.reserve(sizeof(float2) * span * span));
+    float2* lut = lut_in_alloc(ctx->b_lut, n, s);
     launch_build_lut(*scene, n, block, lut, ctx->b_lut_scratch, s);
     WCGH_CUDA(cudaMemcpyAsync(out, lut, sizeof(float2) * span * span, cudaMemcpyDeviceToHost, s));
     sync(s);
@@ -459,15 +462,14 @@ int wcgh_apply_blocks(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int block,
     use_device(ctx);
     cudaStream_t s = ctx->stream;
     const size_t span = size_t(2 * n - 1), n2 = size_t(n) * n;
-    float2* lut = static_cast<float2*>(ctx->b_lut.reserve(sizeof(float2) * span * span));
+    float2* lut = lut_in_alloc(ctx->b_lut, n, s);
     launch_build_lut(*scene, n, block, lut, ctx->b_lut_scratch, s);
-    char* buf = static_cast<char*>(ctx->b_out.reserve(dense.size() * 4 + size_t(m) * 4 + 2 * n2 * 8 + 256));
+    const size_t wbytes = ((dense.size() * 4 + 255) / 256) * 256;
+    char* buf = static_cast<char*>(ctx->b_out.reserve(wbytes + 2 * n2 * 8));
     float* w = reinterpret_cast<float*>(buf);
-    int* row_nnz = reinterpret_cast<int*>(buf + dense.size() * 4);
-    float2* contrib = reinterpret_cast<float2*>(buf + ((dense.size() * 4 + size_t(m) * 4 + 255) / 256) * 256);
+    float2* contrib = reinterpret_cast<float2*>(buf + wbytes);
     WCGH_CUDA(cudaMemcpyAsync(w, dense.data(), dense.size() * 4, cudaMemcpyHostToDevice, s));
-    launch_row_nnz(w, m, row_nnz, s);
-    launch_lut_superpose(lut, n, block, w, m, 0, 0, n, contrib, s, nullptr, row_nnz);
+    launch_lut_dense(lut, n, block, w, m, 0, 0, n, contrib, ctx->cells, ctx->lut_partial, s, nullptr);
     std::vector<float> c(2 * n2);
     WCGH_CUDA(cudaMemcpyAsync(c.data(), contrib, 2 * n2 * 4, cudaMemcpyDeviceToHost, s));
     sync(s);
@@ -495,7 +497,7 @@ int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, 
     const int mr = 2 * m;
     const size_t m2 = size_t(m) * m, r2 = size_t(mr) * mr, n2 = size_t(n) * n;
     const size_t span = size_t(2 * n - 1);
-    float2* lut = static_cast<float2*>(ctx->b_lut.reserve(sizeof(float2) * span * span));
+    float2* lut = lut_in_alloc(ctx->b_lut, n, s);
     launch_build_lut(*scene, n, block, lut, ctx->b_lut_scratch, s);
     char* in = static_cast<char*>(ctx->b_in.reserve((3 * m2 + r2) * 8));
     double* bands = reinterpret_cast<double*>(in);
@@ -505,17 +507,14 @@ int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, 
     WCGH_CUDA(cudaMemcpyAsync(bands + 2 * m2, d, m2 * 8, cudaMemcpyHostToDevice, s));
     WCGH_CUDA(cudaMemcpyAsync(sal, saliency_finer, r2 * 8, cudaMemcpyHostToDevice, s));
     const size_t wbytes = ((r2 * 4 + 255) / 256) * 256, mbytes = ((r2 + 255) / 256) * 256;
-    const size_t nzbytes = ((size_t(mr) * 4 + 255) / 256) * 256;
-    char* o = static_cast<char*>(ctx->b_out.reserve(wbytes + mbytes + nzbytes + 256 + n2 * 8));
+    char* o = static_cast<char*>(ctx->b_out.reserve(wbytes + mbytes + 256 + n2 * 8));
     float* w = reinterpret_cast<float*>(o);
     uint8_t* mask = reinterpret_cast<uint8_t*>(o + wbytes);
-    int* row_nnz = reinterpret_cast<int*>(o + wbytes + mbytes);
-    unsigned long long* count = reinterpret_cast<unsigned long long*>(o + wbytes + mbytes + nzbytes);
-    float2* contrib = reinterpret_cast<float2*>(o + wbytes + mbytes + nzbytes + 256);
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(o + wbytes + mbytes);
+    float2* contrib = reinterpret_cast<float2*>(o + wbytes + mbytes + 256);
     WCGH_CUDA(cudaMemsetAsync(count, 0, 8, s));
     launch_refine_gate(bands, bands + m2, bands + 2 * m2, m, sal, threshold, w, mask, count, s);
-    launch_row_nnz(w, mr, row_nnz, s);
-    launch_lut_superpose(lut, n, block, w, mr, 0, 0, n, contrib, s, nullptr, row_nnz);
+    launch_lut_dense(lut, n, block, w, mr, 0, 0, n, contrib, ctx->cells, ctx->lut_partial, s, nullptr);
     std::vector<float> c(2 * n2);
     unsigned long long gated = 0;
     WCGH_CUDA(cudaMemcpyAsync(c.data(), contrib, 2 * n2 * 4, cudaMemcpyDeviceToHost, s));
@@ -564,17 +563,17 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
       // LUT method: precompute the four block LUTs per layer (reported
       // separately from synthesis, like the reference's lut_build).
       j->w_stage.reserve(sizeof(float) * wstage_len(No) * L);
-      j->row_nnz.reserve(sizeof(int) * (size_t(No) + 64) * 4);
       j->stage_planes.reserve(sizeof(float2) * size_t(d.rows) * d.plane_size * 4);
       const size_t span = size_t(2 * d.plane_size - 1);
       const int blocks[4] = {8, 4, 2, 1};
       for (int l = 0; l < L; ++l) {
         for (int st = 0; st < 4; ++st) {
           auto b = std::make_unique<DevBuf>();
-          b->reserve(sizeof(float2) * span * span);
-          launch_build_lut(d.layers[l], d.plane_size, blocks[st], b->as<float2>(), j->lut_scratch,
+          float2* base = lut_in_alloc(*b, d.plane_size, ctx->stream);
+          launch_build_lut(d.layers[l], d.plane_size, blocks[st], base, j->lut_scratch,
                            ctx->stream);
           j->luts.push_back(std::move(b));
+          j->lut_base.push_back(base);
         }
       }
       sync(ctx->stream);
@@ -706,6 +705,7 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
   require(L == 1, "job (LUT): multi-layer LUT synthesis is not supported yet; use the direct method");
+  j->timing.reset();
   WCGH_CUDA(cudaEventRecord(j->ev[0], s));
   run_analysis(j, s, true);
   const int blocks[4] = {8, 4, 2, 1};
@@ -713,37 +713,47 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   size_t wofs[4];
   wofs[0] = 0;
   for (int st = 1; st < 4; ++st) wofs[st] = wofs[st - 1] + size_t(ms[st - 1]) * ms[st - 1];
-  int* row_nnz = j->row_nnz.as<int>();
-  for (int st = 0; st < 4; ++st)
-    launch_row_nnz(j->w_stage.as<float>() + wofs[st], ms[st], row_nnz + (No + 64) * st, s);
-  j->stats.total_launches += 4;
+  // column-major nonzero cell lists per stage (K2 for the LUT path)
+  for (int st = 0; st < 4; ++st) {
+    launch_stage_cells(j->w_stage.as<float>() + wofs[st], ms[st], j->cells[st], s);
+    WCGH_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(j->h_offsets) + st,
+                              j->cells[st].offsets.as<int>() + ms[st], sizeof(int),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  j->stats.total_launches += 12;
+  WCGH_CUDA(cudaMemcpyAsync(j->h_ops, j->ops.p, sizeof(unsigned long long) * WCGH_OP_LEVELS * L, cudaMemcpyDeviceToHost, s));
+  WCGH_CUDA(cudaMemcpyAsync(j->h_err, j->ops.as<unsigned long long>() + WCGH_OP_LEVELS * L, sizeof(int), cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
+  sync(s);
+  check_analysis_flags(*j->h_err);
+  finish_stats(j, j->h_ops);
+  // the four int counts were written into the int64 staging as ints
+  int nnz[4];
+  std::memcpy(nnz, j->h_offsets, sizeof(nnz));
   const size_t band = size_t(d.rows) * d.plane_size;
   float2* sp = j->stage_planes.as<float2>();
-  double updates = 0;
+  long long cells = 0;
   for (int st = 0; st < 4; ++st) {
-    launch_lut_superpose(j->luts[st]->as<float2>(), d.plane_size, blocks[st],
-                         j->w_stage.as<float>() + wofs[st], ms[st], j->off, d.row0, d.rows,
-                         sp + band * st, s, nullptr, row_nnz + (No + 64) * st);
+    j->stats.total_launches += launch_lut_stage(j->lut_base[st], d.plane_size, blocks[st],
+                                                j->cells[st], nnz[st], j->off, d.row0, d.rows,
+                                                sp + band * st, j->lut_partial, s, &j->timing);
+    cells += nnz[st];
   }
-  j->stats.synth_launches = 4;
-  j->stats.total_launches += 4;
+  j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));
   k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(sp, band, 4, j->plane.as<float2>());
   WCGH_CHECK_LAUNCH();
   j->stats.total_launches += 1;
   WCGH_CUDA(cudaEventRecord(j->ev[3], s));
-  WCGH_CUDA(cudaMemcpyAsync(j->h_ops, j->ops.p, sizeof(unsigned long long) * WCGH_OP_LEVELS * L, cudaMemcpyDeviceToHost, s));
-  WCGH_CUDA(cudaMemcpyAsync(j->h_err, j->ops.as<unsigned long long>() + WCGH_OP_LEVELS * L, sizeof(int), cudaMemcpyDeviceToHost, s));
   sync(s);
-  check_analysis_flags(*j->h_err);
-  finish_stats(j, j->h_ops);
-  (void)updates;
-  j->stats.n_points = -1;
-  j->stats.updates = 0;  // filled by the host mirror from nonzero-weight cell counts
+  // algorithmic updates: (nonzero gated cell, pixel) MACs
+  j->stats.n_points = cells;
+  j->stats.updates = double(cells) * double(d.rows) * double(d.plane_size);
   WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_analysis, j->ev[0], j->ev[1]));
-  WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_synthesis, j->ev[1], j->ev[2]));
-  WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_reduce, j->ev[2], j->ev[3]));
+  j->stats.ms_synthesis = j->timing.elapsed_ms();
+  float synth_phase = 0.f;
+  WCGH_CUDA(cudaEventElapsedTime(&synth_phase, j->ev[1], j->ev[3]));
+  j->stats.ms_reduce = std::max(0.f, synth_phase - j->stats.ms_synthesis);
   WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_total, j->ev[0], j->ev[3]));
 }
 

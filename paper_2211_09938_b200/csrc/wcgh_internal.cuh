@@ -200,15 +200,41 @@ int launch_expand_residual(const double* h, const double* v, const double* d, in
 
 // ---- LUT path (K4 + K5) ------------------------------------------------------
 
+// LUT supports live in guarded allocations: kLutGuardRows zeroed rows before
+// and after the (2n-1)^2 support plus kLutPadCols zeroed tail elements, so
+// the superposition kernel's register window never needs bounds checks.
+constexpr int kLutGuardRows = 96;
+constexpr int kLutPadCols = 256;
+inline size_t lut_alloc_bytes(int n) {
+  const size_t span = size_t(2 * n - 1);
+  return ((span + 2 * kLutGuardRows) * span + kLutPadCols) * sizeof(float2);
+}
+// Zeroes the allocation and returns the pointer to support element (0, 0).
+inline float2* lut_in_alloc(DevBuf& buf, int n, cudaStream_t s) {
+  buf.reserve(lut_alloc_bytes(n));
+  WCGH_CUDA(cudaMemsetAsync(buf.p, 0, lut_alloc_bytes(n), s));
+  return buf.as<float2>() + size_t(kLutGuardRows) * size_t(2 * n - 1);
+}
+
 // Builds the (2n-1)^2 complex64 support of block size B (fp64 sums).
 int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, DevBuf& scratch,
                      cudaStream_t stream);
-// plane rows [row0,row0+rows) of an nh-wide plane += superposition of the
-// m x m dense weight grid w (zero = skip) with LUT support of block B;
-// object grid offset `off` (pixels) on the plane.
-int launch_lut_superpose(const float2* lut, int nh, int block, const float* w, int m, int off,
-                         int row0, int rows, float2* plane, cudaStream_t stream, double* updates,
-                         const int* row_nnz);
-int launch_row_nnz(const float* w, int m, int* row_nnz, cudaStream_t stream);
+// Column-major list of the nonzero weights of one stage's m x m cell grid:
+// entries (c_y, w bits) grouped by cell column, offsets[c_x]..offsets[c_x+1].
+struct StageCells {
+  int m = 0;
+  DevBuf counts, offsets, entries;
+};
+int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t stream);
+// out (rows x nh complex64, overwritten) = superposition of the stage's `nnz`
+// listed cells with the block-B LUT; object grid offset `off` on the plane.
+int launch_lut_stage(const float2* lut, int nh, int block, const StageCells& sc, int nnz,
+                     int off, int row0, int rows, float2* out, DevBuf& partial,
+                     cudaStream_t stream, DirectTiming* timing);
+// Dense weight grid convenience: builds the list, reads nnz (synchronizes),
+// superposes.
+int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,
+                     int row0, int rows, float2* out, StageCells& sc, DevBuf& partial,
+                     cudaStream_t stream, long long* nnz_out);
 
 }  // namespace wcgh
