@@ -76,10 +76,12 @@ struct wcgh_job {
   int64_t* h_offsets = nullptr;       // n_layers + 1
   unsigned long long* h_ops = nullptr;  // n_layers * 5
   int* h_err = nullptr;
+  int* h_tot = nullptr;  // LUT: (runs, dense steps, nnz) per stage
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   wcgh_stats stats{};
   bool uploaded = false;
   ~wcgh_job() {
+    if (h_tot) cudaFreeHost(h_tot);
     if (h_offsets) cudaFreeHost(h_offsets);
     if (h_ops) cudaFreeHost(h_ops);
     if (h_err) cudaFreeHost(h_err);
@@ -556,6 +558,7 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     WCGH_CUDA(cudaMallocHost(&j->h_offsets, sizeof(int64_t) * (L + 1)));
     WCGH_CUDA(cudaMallocHost(&j->h_ops, sizeof(unsigned long long) * WCGH_OP_LEVELS * L));
     WCGH_CUDA(cudaMallocHost(&j->h_err, sizeof(int) * 4));
+    WCGH_CUDA(cudaMallocHost(&j->h_tot, sizeof(int) * 16));
     for (auto& e : j->ev) WCGH_CUDA(cudaEventCreate(&e));
     if (d.method == WCGH_METHOD_DIRECT) {
       j->points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1));
@@ -715,29 +718,27 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   for (int st = 1; st < 4; ++st) wofs[st] = wofs[st - 1] + size_t(ms[st - 1]) * ms[st - 1];
   // column-major nonzero cell lists per stage (K2 for the LUT path)
   for (int st = 0; st < 4; ++st) {
-    launch_stage_cells(j->w_stage.as<float>() + wofs[st], ms[st], j->cells[st], s);
-    WCGH_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(j->h_offsets) + st,
-                              j->cells[st].offsets.as<int>() + ms[st], sizeof(int),
-                              cudaMemcpyDeviceToHost, s));
+    j->stats.total_launches += launch_stage_cells(j->w_stage.as<float>() + wofs[st], ms[st], j->cells[st], s);
+    stage_cells_totals_async(j->cells[st], j->h_tot + 3 * st, s);
   }
-  j->stats.total_launches += 12;
   WCGH_CUDA(cudaMemcpyAsync(j->h_ops, j->ops.p, sizeof(unsigned long long) * WCGH_OP_LEVELS * L, cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaMemcpyAsync(j->h_err, j->ops.as<unsigned long long>() + WCGH_OP_LEVELS * L, sizeof(int), cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
   sync(s);
   check_analysis_flags(*j->h_err);
   finish_stats(j, j->h_ops);
-  // the four int counts were written into the int64 staging as ints
-  int nnz[4];
-  std::memcpy(nnz, j->h_offsets, sizeof(nnz));
   const size_t band = size_t(d.rows) * d.plane_size;
   float2* sp = j->stage_planes.as<float2>();
   long long cells = 0;
   for (int st = 0; st < 4; ++st) {
-    j->stats.total_launches += launch_lut_stage(j->lut_base[st], d.plane_size, blocks[st],
-                                                j->cells[st], nnz[st], j->off, d.row0, d.rows,
-                                                sp + band * st, j->lut_partial, s, &j->timing);
-    cells += nnz[st];
+    StageCells& sc = j->cells[st];
+    sc.n_runs = j->h_tot[3 * st];
+    sc.n_dense = j->h_tot[3 * st + 1];
+    sc.nnz = j->h_tot[3 * st + 2];
+    j->stats.total_launches += launch_lut_stage(j->lut_base[st], d.plane_size, blocks[st], sc,
+                                                j->off, d.row0, d.rows, sp + band * st,
+                                                j->lut_partial, s, &j->timing);
+    cells += sc.nnz;
   }
   j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));

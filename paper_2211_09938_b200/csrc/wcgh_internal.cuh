@@ -219,18 +219,23 @@ inline float2* lut_in_alloc(DevBuf& buf, int n, cudaStream_t s) {
 // Builds the (2n-1)^2 complex64 support of block size B (fp64 sums).
 int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, DevBuf& scratch,
                      cudaStream_t stream);
-// Column-major list of the nonzero weights of one stage's m x m cell grid:
-// entries (c_y, w bits) grouped by cell column, offsets[c_x]..offsets[c_x+1].
+// Run lists of one stage's m x m cell grid (column-major): runs of nonzero
+// cells (gaps <= the kernel's window height stepped through) as int4
+// (c_x, c_y start, steps, dense offset) plus the dense per-step weights.
+// Host totals (n_runs, n_dense, nnz) are filled after stage_cells_totals_async
+// has completed.
 struct StageCells {
   int m = 0;
-  DevBuf counts, offsets, entries;
+  int n_runs = 0, n_dense = 0, nnz = 0;
+  DevBuf counts, offsets, runs, dense;
 };
 int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t stream);
-// out (rows x nh complex64, overwritten) = superposition of the stage's `nnz`
+void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t stream);
+// out (rows x nh complex64, overwritten) = superposition of the stage's
 // listed cells with the block-B LUT; object grid offset `off` on the plane.
-int launch_lut_stage(const float2* lut, int nh, int block, const StageCells& sc, int nnz,
-                     int off, int row0, int rows, float2* out, DevBuf& partial,
-                     cudaStream_t stream, DirectTiming* timing);
+int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
+                     int rows, float2* out, DevBuf& partial, cudaStream_t stream,
+                     DirectTiming* timing);
 // Dense weight grid convenience: builds the list, reads nnz (synchronizes),
 // superposes.
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,

@@ -70,53 +70,110 @@ __global__ void k_box_sum(const double2* __restrict__ base, int ext, int span, i
   lut[i] = make_float2(float(sr), float(si));
 }
 
-// Column-major compaction of a dense m x m weight grid: one warp per cell
-// column, ascending c_y, nonzero weights only.
-__global__ void k_col_counts(const float* __restrict__ w, int m, int* __restrict__ cnt) {
+// Run lists of a dense m x m weight grid (one warp per cell column c_x):
+// nonzero cells in ascending c_y are grouped into runs whose consecutive
+// gaps are <= R (the superposition kernel steps through such gaps with its
+// register window); each run gets a record (c_x, c_y start, length, offset
+// into a dense weight array holding every step's weight, zeros in gaps).
+__global__ void k_runs_count(const float* __restrict__ w, int m, int R, int* __restrict__ n_runs,
+                             int* __restrict__ n_dense, int* __restrict__ n_nnz) {
   const int lane = threadIdx.x & 31;
   const int cx = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (cx >= m) return;
-  int c = 0;
-  for (int cy = lane; cy < m; cy += 32) c += w[size_t(cy) * m + cx] != 0.0f;
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-  if (lane == 0) cnt[cx] = c;
-}
-
-__global__ void k_col_fill(const float* __restrict__ w, int m, const int* __restrict__ off,
-                           int2* __restrict__ ent) {
-  const int lane = threadIdx.x & 31;
-  const int cx = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (cx >= m) return;
-  int pos = off[cx];
+  int last = -(1 << 29), runs = 0, dense = 0, nnz = 0, start = 0;
   for (int base = 0; base < m; base += 32) {
     const int cy = base + lane;
     const float v = cy < m ? w[size_t(cy) * m + cx] : 0.0f;
-    const unsigned b = __ballot_sync(kFull, v != 0.0f);
-    if (v != 0.0f) ent[pos + __popc(b & ((1u << lane) - 1u))] = make_int2(cy, __float_as_int(v));
-    pos += __popc(b);
+    unsigned mask = __ballot_sync(kFull, v != 0.0f);
+    while (mask) {
+      const int c = base + __ffs(mask) - 1;
+      mask &= mask - 1;
+      ++nnz;
+      if (c - last > R) {
+        if (runs) dense += last - start + 1;
+        ++runs;
+        start = c;
+      }
+      last = c;
+    }
+  }
+  if (runs) dense += last - start + 1;
+  if (lane == 0) {
+    n_runs[cx] = runs;
+    n_dense[cx] = dense;
+    n_nnz[cx] = nnz;
   }
 }
 
-constexpr int kThreads = 256;
+__global__ void k_runs_fill(const float* __restrict__ w, int m, int R, const int* __restrict__ run_off,
+                            const int* __restrict__ dense_off, int4* __restrict__ runs,
+                            float* __restrict__ dense) {
+  const int lane = threadIdx.x & 31;
+  const int cx = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (cx >= m) return;
+  int rp = run_off[cx], dp = dense_off[cx];
+  int cur = -1, start = 0, last = -(1 << 29), wofs = 0;
+  for (int base = 0; base < m; base += 32) {
+    const int cy = base + lane;
+    const float v = cy < m ? w[size_t(cy) * m + cx] : 0.0f;
+    unsigned mask = __ballot_sync(kFull, v != 0.0f);
+    while (mask) {
+      const int b = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int c = base + b;
+      const float vc = __shfl_sync(kFull, v, b);
+      if (c - last > R) {  // a new run
+        if (cur >= 0) {
+          if (lane == 0) runs[cur].z = last - start + 1;
+          dp = wofs + (last - start + 1);
+        }
+        cur = rp++;
+        start = c;
+        wofs = dp;
+        if (lane == 0) runs[cur] = make_int4(cx, c, 0, wofs);
+      }
+      if (lane == 0) dense[wofs + (c - start)] = vc;
+      last = c;
+    }
+  }
+  if (cur >= 0 && lane == 0) runs[cur].z = last - start + 1;
+}
 
-// Dynamic shared memory: the chunk's column-major entries (cy, w bits).
-template <int B, int R, int PX, int D>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_lut_stage(const float2* __restrict__ lut, int nh, const int* __restrict__ col_off,
-                const int2* __restrict__ ent, int m, int off, int row0, int rows, int tiles_x,
-                int chunk0, int chunk_entries, int nnz, float2* __restrict__ out,
+template <int B, int R, int PX, int D, int W>
+__global__ void __launch_bounds__(W * 32, 3)
+    k_lut_stage(const float2* __restrict__ lut, int nh, const int4* __restrict__ runs,
+                int n_runs, const float* __restrict__ dense, int off, int row0, int rows,
+                int tiles_x, int chunk0, int chunk_steps, float2* __restrict__ out,
                 size_t out_stride) {
-  extern __shared__ int2 s_ent[];
-  constexpr int BW = B < 8 ? B : 8;  // row residues spread over the 8 warps
-  constexpr int S = R + D;           // ring: R live diagonals + D prefetched
+  extern __shared__ float s_w[];
+  constexpr int S = R + D;  // ring: R live diagonals + D prefetched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = warp % BW, q = warp / BW;
-  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-  const int yb = ty * (8 * R) + q * (R * B) + r;  // band row of pixel row j = 0
+  const int tx = blockIdx.x % tiles_x, tyc = blockIdx.x / tiles_x;
+  const int rw = tyc * W + warp;          // row-warp: R rows at stride B
+  const int yb = (rw / B) * (B * R) + rw % B;  // band row of pixel row 0
   const int x0 = tx * (32 * PX) + lane;
   const int span = 2 * nh - 1;
-  const int e_lo = (chunk0 + blockIdx.y) * chunk_entries;
-  const int e_hi = min(e_lo + chunk_entries, nnz);
+  const int d_lo = (chunk0 + blockIdx.y) * chunk_steps;
+  const int d_hi = d_lo + chunk_steps;
+
+  // runs starting in [d_lo, d_hi) of the dense step array (runs are ordered by offset)
+  auto lower_bound = [&](int key) {
+    int lo = 0, hi = n_runs;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(&runs[mid].w) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const int r_lo = lower_bound(d_lo), r_hi = lower_bound(d_hi);
+  int w_lo = 0;
+  if (r_lo < r_hi) {
+    w_lo = __ldg(&runs[r_lo].w);
+    const int4 lr = __ldg(runs + r_hi - 1);
+    const int w_n = lr.w + lr.z - w_lo;
+    for (int i = threadIdx.x; i < w_n; i += W * 32) s_w[i] = __ldg(dense + w_lo + i);
+  }
+  __syncthreads();
 
   float2 acc[R][PX];
 #pragma unroll
@@ -124,94 +181,59 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int i = 0; i < PX; ++i) acc[j][i] = make_float2(0.f, 0.f);
 
-  for (int e = e_lo + threadIdx.x; e < e_hi; e += kThreads) s_ent[e - e_lo] = __ldg(ent + e);
-  __syncthreads();
-
-  if (e_lo < e_hi) {
-    // first cell column of the chunk: col_off[cx] <= e_lo < col_off[cx + 1]
-    int lo = 0, hi = m;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(col_off + mid) <= e_lo) lo = mid; else hi = mid;
-    }
-    // LUT row of pixel row j at cell row cy: (row0 + yb + jB) - off - B cy + nh - 1.
-    // `lut` points into a guarded allocation (kLutGuardRows rows before and
-    // after, kLutPadCols elements of tail padding), so the window and the
-    // prefetch never need clamping; out-of-plane pixels read guard data and
-    // are never stored.
-    const int rho_base = row0 + yb - off + nh - 1;
-    const long long row_step = (long long)B * span;  // one cell row down the LUT
-    int ce_prev = __ldg(col_off + lo);
-    for (int cx = lo; cx < m; ++cx) {
-      const int ce_abs = __ldg(col_off + cx + 1);
-      const int cb = max(ce_prev, e_lo) - e_lo;
-      const int ce = min(ce_abs, e_hi) - e_lo;
-      ce_prev = ce_abs;
-      if (cb >= e_hi - e_lo) break;
-      if (cb >= ce) continue;
-      const float2* cp = lut + (x0 - off - B * cx + nh - 1);  // this thread's column 0
-      int k = cb;
-      while (k < ce) {
-        // run: entries k..k_end-1 whose consecutive cy gaps are <= R
-        int k_end = k + 1;
-        int cy_prev = s_ent[k].x;
-        while (k_end < ce) {
-          const int cy_n = s_ent[k_end].x;
-          if (cy_n - cy_prev > R) break;
-          cy_prev = cy_n;
-          ++k_end;
-        }
-        const int cy_s = s_ent[k].x;
-        const int n_steps = cy_prev - cy_s + 1;
-        // ring slot (t mod S) holds diagonal t: LUT row rho0 + B t
-        const float2* rp = cp + (long long)(rho_base - B * cy_s) * span;
-        float2 ring[S][PX];
-        {
-          const float2* rt = rp - D * row_step;
+  // LUT row of pixel row j at cell row cy: (row0 + yb + jB) - off - B cy + nh - 1.
+  // `lut` points into a guarded allocation (kLutGuardRows rows before and
+  // after, kLutPadCols elements of tail padding), so the window and the
+  // prefetch never need clamping; out-of-plane pixels read guard data and
+  // are never stored.
+  const int rho_base = row0 + yb - off + nh - 1;
+  const long long row_step = (long long)B * span;  // one cell row down the LUT
+  for (int ri = r_lo; ri < r_hi; ++ri) {
+    const int4 run = __ldg(runs + ri);  // (c_x, c_y start, steps, dense offset)
+    const int cx = run.x, cy_s = run.y, n_steps = run.z;
+    const float* ws = s_w + (run.w - w_lo);
+    const float2* rp = lut + (x0 - off - B * cx + nh - 1) + (long long)(rho_base - B * cy_s) * span;
+    // ring slot (t mod S) holds diagonal t: LUT row rho0 + B t
+    float2 ring[S][PX];
+    {
+      const float2* rt = rp - D * row_step;
 #pragma unroll
-          for (int t = -D; t < R; ++t) {
+      for (int t = -D; t < R; ++t) {
 #pragma unroll
-            for (int i = 0; i < PX; ++i) ring[(t + S) % S][i] = __ldg(rt + 32 * i);
-            rt += row_step;
-          }
-        }
-        // prefetch pointer: diagonal -(D + 1), then one row lower per step
-        const float2* pf = rp - (D + 1) * row_step;
-        int2 nx = s_ent[k];
-        int cy = cy_s;
-        const int full = n_steps - n_steps % S;
-        // one step: MAC if cell (cx, cy) is listed, then refill the dead slot
-#define WCGH_LUT_STEP(uu)                                                          \
-  {                                                                                \
-    if (nx.x == cy) {                                                              \
-      const float wv = __int_as_float(nx.y);                                       \
-      ++k;                                                                         \
-      nx = k < k_end ? s_ent[k] : make_int2(-1, 0);                                \
-      _Pragma("unroll") for (int j = 0; j < R; ++j)                                \
-      _Pragma("unroll") for (int i = 0; i < PX; ++i) {                             \
-        const float2 v = ring[(j - (uu) + 2 * S) % S][i];                          \
-        acc[j][i].x = fmaf(wv, v.x, acc[j][i].x);                                  \
-        acc[j][i].y = fmaf(wv, v.y, acc[j][i].y);                                  \
-      }                                                                            \
-    }                                                                              \
-    _Pragma("unroll") for (int i = 0; i < PX; ++i)                                 \
-      ring[(R - 1 - (uu) + S) % S][i] = __ldg(pf + 32 * i);                        \
-    pf -= row_step;                                                                \
-    ++cy;                                                                          \
-  }
-        for (int ub = 0; ub < full; ub += S) {
-#pragma unroll
-          for (int uu = 0; uu < S; ++uu) WCGH_LUT_STEP(uu)
-        }
-#pragma unroll
-        for (int uu = 0; uu < S - 1; ++uu) {
-          if (full + uu < n_steps) WCGH_LUT_STEP(uu)
-        }
-#undef WCGH_LUT_STEP
-        k = k_end;
+        for (int i = 0; i < PX; ++i) ring[(t + S) % S][i] = __ldg(rt + 32 * i);
+        rt += row_step;
       }
     }
+    // prefetch pointer: diagonal -(D + 1), then one row lower per step
+    const float2* pf = rp - (D + 1) * row_step;
+    // one step: MAC the listed weight (zero in gaps), then refill the dead slot
+#define WCGH_LUT_STEP(uu, u)                                                    \
+  {                                                                             \
+    const float wv = ws[u];                                                     \
+    if (wv != 0.f) {                                                            \
+      _Pragma("unroll") for (int j = 0; j < R; ++j)                             \
+      _Pragma("unroll") for (int i = 0; i < PX; ++i) {                          \
+        const float2 v = ring[(j - (uu) + 2 * S) % S][i];                       \
+        acc[j][i].x = fmaf(wv, v.x, acc[j][i].x);                               \
+        acc[j][i].y = fmaf(wv, v.y, acc[j][i].y);                               \
+      }                                                                         \
+    }                                                                           \
+    _Pragma("unroll") for (int i = 0; i < PX; ++i)                              \
+      ring[(R - 1 - (uu) + S) % S][i] = __ldg(pf + 32 * i);                     \
+    pf -= row_step;                                                             \
   }
+    const int full = n_steps - n_steps % S;
+    for (int ub = 0; ub < full; ub += S) {
+#pragma unroll
+      for (int uu = 0; uu < S; ++uu) WCGH_LUT_STEP(uu, ub + uu)
+    }
+#pragma unroll
+    for (int uu = 0; uu < S - 1; ++uu) {
+      if (full + uu < n_steps) WCGH_LUT_STEP(uu, full + uu)
+    }
+#undef WCGH_LUT_STEP
+  }
+
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int row = yb + j * B;
@@ -244,16 +266,18 @@ __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, siz
   out[i] = make_float2(float(re), float(im));
 }
 
-constexpr int kR = 8, kPX = 2, kD = 2;
-constexpr int kMaxChunkEntries = 4096;
+constexpr int kR = 8, kPX = 4, kD = 2, kW = 4;
+constexpr int kMaxChunkSteps = 4096;
 constexpr size_t kPartialBytes = 2ull << 30;
 
 template <int B>
-void launch_stage_b(const float2* lut, int nh, const int* col_off, const int2* ent, int m,
-                    int off, int row0, int rows, int tiles_x, dim3 grid, int chunk0,
-                    int chunk_entries, int nnz, float2* out, size_t stride, cudaStream_t s) {
-  k_lut_stage<B, kR, kPX, kD><<<grid, kThreads, sizeof(int2) * chunk_entries, s>>>(
-      lut, nh, col_off, ent, m, off, row0, rows, tiles_x, chunk0, chunk_entries, nnz, out, stride);
+void launch_stage_b(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
+                    int tiles_x, dim3 grid, int chunk0, int chunk_steps, float2* out,
+                    size_t stride, cudaStream_t s) {
+  const size_t smem = sizeof(float) * size_t(chunk_steps + sc.m + 32);
+  k_lut_stage<B, kR, kPX, kD, kW><<<grid, kW * 32, smem, s>>>(
+      lut, nh, sc.runs.as<int4>(), sc.n_runs, sc.dense.as<float>(), off, row0, rows, tiles_x,
+      chunk0, chunk_steps, out, stride);
 }
 
 }  // namespace
@@ -278,46 +302,54 @@ int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, Dev
 
 int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t s) {
   sc.m = m;
-  int* cnt = static_cast<int*>(sc.counts.reserve(sizeof(int) * (size_t(m) + 1)));
-  int* off = static_cast<int*>(sc.offsets.reserve(sizeof(int) * (size_t(m) + 1)));
-  sc.entries.reserve(sizeof(int2) * size_t(m) * m);
+  int* c = static_cast<int*>(sc.counts.reserve(sizeof(int) * 3 * (size_t(m) + 1)));
+  int* o = static_cast<int*>(sc.offsets.reserve(sizeof(int) * 3 * (size_t(m) + 1)));
+  const size_t mm = size_t(m) * m;
+  sc.runs.reserve(sizeof(int4) * (mm + 1));
+  sc.dense.reserve(sizeof(float) * (mm + 1));
+  WCGH_CUDA(cudaMemsetAsync(sc.dense.p, 0, sizeof(float) * (mm + 1), s));
   const unsigned g = unsigned((m + 7) / 8);
-  k_col_counts<<<g, 256, 0, s>>>(w, m, cnt);
+  k_runs_count<<<g, 256, 0, s>>>(w, m, kR, c, c + (m + 1), c + 2 * (m + 1));
   WCGH_CHECK_LAUNCH();
-  launch_scan(cnt, off, m, s);
-  k_col_fill<<<g, 256, 0, s>>>(w, m, off, sc.entries.as<int2>());
+  for (int k = 0; k < 3; ++k) launch_scan(c + k * (m + 1), o + k * (m + 1), m, s);
+  k_runs_fill<<<g, 256, 0, s>>>(w, m, kR, o, o + (m + 1), sc.runs.as<int4>(), sc.dense.as<float>());
   WCGH_CHECK_LAUNCH();
-  return 3;
+  return 5;
 }
 
-int launch_lut_stage(const float2* lut, int nh, int block, const StageCells& sc, int nnz,
-                     int off, int row0, int rows, float2* out, DevBuf& partial, cudaStream_t s,
-                     DirectTiming* timing) {
+void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t s) {
+  const int m = sc.m;
+  const int* o = sc.offsets.as<int>();
+  for (int k = 0; k < 3; ++k)
+    WCGH_CUDA(cudaMemcpyAsync(host3 + k, o + k * (m + 1) + m, sizeof(int), cudaMemcpyDeviceToHost, s));
+}
+
+int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
+                     int rows, float2* out, DevBuf& partial, cudaStream_t s, DirectTiming* timing) {
   const size_t band = size_t(rows) * nh;
-  if (nnz == 0) {
+  if (sc.n_runs == 0) {
     WCGH_CUDA(cudaMemsetAsync(out, 0, band * sizeof(float2), s));
     return 0;
   }
-  // chunk size depends on nnz only (never on the row band): ~48+ chunks
-  int chunk_entries = std::min(kMaxChunkEntries, std::max(256, (nnz + 47) / 48));
-  chunk_entries = (chunk_entries + 127) / 128 * 128;
-  const int n_chunks = (nnz + chunk_entries - 1) / chunk_entries;
+  // chunk size depends on the stage's step count only (never on the row band)
+  int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + 47) / 48));
+  chunk_steps = (chunk_steps + 127) / 128 * 128;
+  const int n_chunks = (sc.n_dense + chunk_steps - 1) / chunk_steps;
   const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
   float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
   const int tiles_x = (nh + 32 * kPX - 1) / (32 * kPX);
-  const int tiles_y = (rows + 8 * kR - 1) / (8 * kR);
-  const int* col_off = sc.offsets.as<int>();
-  const int2* ent = sc.entries.as<int2>();
+  const int row_warps = (rows + block * kR - 1) / (block * kR) * block;
+  const int tiles_y = (row_warps + kW - 1) / kW;
   int launches = 0;
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
     const int ng = std::min(group, n_chunks - g0);
     dim3 grid(unsigned(tiles_x * tiles_y), unsigned(ng));
     if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), s));
     switch (block) {
-      case 1: launch_stage_b<1>(lut, nh, col_off, ent, sc.m, off, row0, rows, tiles_x, grid, g0, chunk_entries, nnz, part, band, s); break;
-      case 2: launch_stage_b<2>(lut, nh, col_off, ent, sc.m, off, row0, rows, tiles_x, grid, g0, chunk_entries, nnz, part, band, s); break;
-      case 4: launch_stage_b<4>(lut, nh, col_off, ent, sc.m, off, row0, rows, tiles_x, grid, g0, chunk_entries, nnz, part, band, s); break;
-      case 8: launch_stage_b<8>(lut, nh, col_off, ent, sc.m, off, row0, rows, tiles_x, grid, g0, chunk_entries, nnz, part, band, s); break;
+      case 1: launch_stage_b<1>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 2: launch_stage_b<2>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 4: launch_stage_b<4>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 8: launch_stage_b<8>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
       default: throw ValidationError("LUT superposition: unsupported block size");
     }
     WCGH_CHECK_LAUNCH();
@@ -332,12 +364,15 @@ int launch_lut_stage(const float2* lut, int nh, int block, const StageCells& sc,
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,
                      int row0, int rows, float2* out, StageCells& sc, DevBuf& partial,
                      cudaStream_t s, long long* nnz_out) {
-  launch_stage_cells(w, m, sc, s);
-  int nnz = 0;
-  WCGH_CUDA(cudaMemcpyAsync(&nnz, sc.offsets.as<int>() + m, sizeof(int), cudaMemcpyDeviceToHost, s));
+  int launches = launch_stage_cells(w, m, sc, s);
+  int tot[3];
+  stage_cells_totals_async(sc, tot, s);
   WCGH_CUDA(cudaStreamSynchronize(s));
-  if (nnz_out) *nnz_out = nnz;
-  return 4 + launch_lut_stage(lut, nh, block, sc, nnz, off, row0, rows, out, partial, s, nullptr);
+  sc.n_runs = tot[0];
+  sc.n_dense = tot[1];
+  sc.nnz = tot[2];
+  if (nnz_out) *nnz_out = sc.nnz;
+  return launches + launch_lut_stage(lut, nh, block, sc, off, row0, rows, out, partial, s, nullptr);
 }
 
 }  // namespace wcgh
