@@ -226,6 +226,7 @@ int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, Dev
 // has completed.
 struct StageCells {
   int m = 0;
+  int gap = 0;  // run gap threshold (the window height R) the lists were built with
   int n_runs = 0, n_dense = 0, nnz = 0;
   DevBuf counts, offsets, runs, dense;
 };

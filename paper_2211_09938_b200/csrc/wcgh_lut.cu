@@ -29,6 +29,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "wcgh_internal.cuh"
@@ -266,18 +268,62 @@ __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, siz
   out[i] = make_float2(float(re), float(im));
 }
 
-constexpr int kR = 8, kPX = 4, kD = 2, kW = 4;
+constexpr int kW = 4;  // warps per CTA
 constexpr int kMaxChunkSteps = 4096;
 constexpr size_t kPartialBytes = 2ull << 30;
 
-template <int B>
-void launch_stage_b(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
+// Register-window shape (R rows x PX columns per thread, D rows of prefetch).
+// Default 8 x 4 x 2; WCGH_LUT_VARIANT="R,PX,D" selects another compiled shape
+// (tuning only; results are identical up to fp32 summation order).
+struct LutVariant {
+  int R, PX, D;
+};
+LutVariant lut_variant() {
+  static const LutVariant v = [] {
+    LutVariant d{8, 4, 2};
+    if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
+      int r = 0, px = 0, dd = 0;
+      if (std::sscanf(e, "%d,%d,%d", &r, &px, &dd) == 3) d = LutVariant{r, px, dd};
+    }
+    return d;
+  }();
+  return v;
+}
+int lut_chunk_target() {
+  static const int t = [] {
+    const char* e = std::getenv("WCGH_LUT_CHUNKS");
+    return e ? std::max(1, std::atoi(e)) : 24;
+  }();
+  return t;
+}
+
+template <int B, int R, int PX, int D>
+void launch_stage_v(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
                     int tiles_x, dim3 grid, int chunk0, int chunk_steps, float2* out,
                     size_t stride, cudaStream_t s) {
   const size_t smem = sizeof(float) * size_t(chunk_steps + sc.m + 32);
-  k_lut_stage<B, kR, kPX, kD, kW><<<grid, kW * 32, smem, s>>>(
+  k_lut_stage<B, R, PX, D, kW><<<grid, kW * 32, smem, s>>>(
       lut, nh, sc.runs.as<int4>(), sc.n_runs, sc.dense.as<float>(), off, row0, rows, tiles_x,
       chunk0, chunk_steps, out, stride);
+}
+
+template <int B>
+void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageCells& sc, int off,
+                    int row0, int rows, int tiles_x, dim3 grid, int chunk0, int chunk_steps,
+                    float2* out, size_t stride, cudaStream_t s) {
+#define WCGH_V(R_, PX_, D_)                                                                  \
+  if (v.R == R_ && v.PX == PX_ && v.D == D_) {                                               \
+    launch_stage_v<B, R_, PX_, D_>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,     \
+                                   chunk_steps, out, stride, s);                             \
+    return;                                                                                  \
+  }
+  WCGH_V(8, 4, 2)
+  WCGH_V(16, 2, 2)
+  WCGH_V(16, 2, 4)
+  WCGH_V(8, 2, 4)
+  WCGH_V(12, 2, 4)
+#undef WCGH_V
+  throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
 }
 
 }  // namespace
@@ -309,10 +355,12 @@ int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t s) {
   sc.dense.reserve(sizeof(float) * (mm + 1));
   WCGH_CUDA(cudaMemsetAsync(sc.dense.p, 0, sizeof(float) * (mm + 1), s));
   const unsigned g = unsigned((m + 7) / 8);
-  k_runs_count<<<g, 256, 0, s>>>(w, m, kR, c, c + (m + 1), c + 2 * (m + 1));
+  const int R = lut_variant().R;
+  sc.gap = R;
+  k_runs_count<<<g, 256, 0, s>>>(w, m, R, c, c + (m + 1), c + 2 * (m + 1));
   WCGH_CHECK_LAUNCH();
   for (int k = 0; k < 3; ++k) launch_scan(c + k * (m + 1), o + k * (m + 1), m, s);
-  k_runs_fill<<<g, 256, 0, s>>>(w, m, kR, o, o + (m + 1), sc.runs.as<int4>(), sc.dense.as<float>());
+  k_runs_fill<<<g, 256, 0, s>>>(w, m, R, o, o + (m + 1), sc.runs.as<int4>(), sc.dense.as<float>());
   WCGH_CHECK_LAUNCH();
   return 5;
 }
@@ -332,13 +380,16 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
     return 0;
   }
   // chunk size depends on the stage's step count only (never on the row band)
-  int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + 47) / 48));
+  const LutVariant v = lut_variant();
+  require(sc.gap == v.R, "LUT superposition: run lists built for another window height");
+  const int target = lut_chunk_target();
+  int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + target - 1) / target));
   chunk_steps = (chunk_steps + 127) / 128 * 128;
   const int n_chunks = (sc.n_dense + chunk_steps - 1) / chunk_steps;
   const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
   float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
-  const int tiles_x = (nh + 32 * kPX - 1) / (32 * kPX);
-  const int row_warps = (rows + block * kR - 1) / (block * kR) * block;
+  const int tiles_x = (nh + 32 * v.PX - 1) / (32 * v.PX);
+  const int row_warps = (rows + block * v.R - 1) / (block * v.R) * block;
   const int tiles_y = (row_warps + kW - 1) / kW;
   int launches = 0;
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
@@ -346,10 +397,10 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
     dim3 grid(unsigned(tiles_x * tiles_y), unsigned(ng));
     if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), s));
     switch (block) {
-      case 1: launch_stage_b<1>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
-      case 2: launch_stage_b<2>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
-      case 4: launch_stage_b<4>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
-      case 8: launch_stage_b<8>(lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 1: launch_stage_b<1>(v, lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 2: launch_stage_b<2>(v, lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 4: launch_stage_b<4>(v, lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
+      case 8: launch_stage_b<8>(v, lut, nh, sc, off, row0, rows, tiles_x, grid, g0, chunk_steps, part, band, s); break;
       default: throw ValidationError("LUT superposition: unsupported block size");
     }
     WCGH_CHECK_LAUNCH();
