@@ -463,9 +463,19 @@ def main():
             bound = "fp32"
             dram = int(4 * (2 * c.plane_size - 1) ** 2 * 8 + rows * c.plane_size * 8)
         peak = SM_COUNT * f_max * per_clk
+        # dram__bytes_read + dram__bytes_write per launch from the committed
+        # `ncu --set full` capture (profiles/, tools/profile_round.sh)
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("k_direct_fixed" if bound == "sfu" else "k_lut_stage")
         roof = {
             "bound": bound, "achieved": achieved, "peak": peak, "unit": UNIT,
-            "frac": achieved / peak, "traffic": None, "kernel": kernel, "kernel_ms": k_ms,
+            "frac": achieved / peak, "traffic": traffic, "kernel": kernel, "kernel_ms": k_ms,
+            "traffic_note": ("bytes per launch from profiles/ncu_traffic.json (config-1 capture for K3; "
+                             "config-2 stage average for K4); dominated by the fixed-order "
+                             "partial-sum planes, not by point/LUT reads"),
             "peak_basis": basis,
             "frac_at_measured_clock": (achieved / (SM_COUNT * f_meas * per_clk) if f_meas else None),
             "dram_bytes_per_step_algorithmic": dram,

@@ -1,0 +1,147 @@
+// Drop-in check: the reference's own C++ API (namespace wavecgh, reference
+// headers and types) backed by integration/wavecgh_gpu.cpp + libwcgh.so,
+// compared with the unmodified CPU reference (oracle/_ref, namespace
+// wavecgh_ref, through its C shim). Exit code 0 = all checks passed.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "wavecgh/errors.hpp"
+#include "wavecgh/fringe_lut.hpp"
+#include "wavecgh/haar.hpp"
+#include "wavecgh/saliency.hpp"
+#include "wavecgh/synthesis.hpp"
+
+extern "C" {
+int ref_haar_analyze(const double* image, int n, int levels, double* out);
+int ref_quantize_saliency(const double* sal, int n, double* out);
+int ref_synthesize_progressive(const double* object, const double* saliency, int n, double wl,
+                               double pitch, double z, const double* thresholds,
+                               const int* enables, int workers, int use_seed, std::uint64_t seed,
+                               double* planes_out, std::uint8_t* masks_out, std::uint64_t* ops_out);
+int ref_synthesize_pointwise_oracle(const double* object, int n, double wl, double pitch, double z,
+                                    int workers, double* out, std::uint64_t* ops);
+int ref_random_image(int w, int h, std::uint64_t seed, double* out);
+int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx, int cy,
+                    double w_re, double w_im, double* plane, std::uint64_t* ops);
+}
+
+using namespace wavecgh;
+
+static int failures = 0;
+#define EXPECT(cond, ...)                        \
+  do {                                           \
+    if (!(cond)) {                               \
+      std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+      std::printf(__VA_ARGS__);                  \
+      std::printf("\n");                         \
+      ++failures;                                \
+    }                                            \
+  } while (0)
+
+static RealImage random_image(int n, std::uint64_t seed) {
+  std::vector<double> v(std::size_t(n) * n);
+  ref_random_image(n, n, seed, v.data());
+  return RealImage(n, n, std::move(v));
+}
+
+static double rel_l2(const ComplexField& a, const double* ref) {
+  double num = 0, den = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    const std::complex<double> r(ref[2 * i], ref[2 * i + 1]);
+    num += std::norm(a.data()[i] - r);
+    den += std::norm(r);
+  }
+  return std::sqrt(num / den);
+}
+
+int main() {
+  const double wl = 532e-9, pitch = 8e-6, z = 0.1;
+  for (int n : {16, 32, 64}) {
+    const RealImage object = random_image(n, 900 + n);
+    const RealImage saliency = random_image(n, 77 + n);
+    // haar_analyze and quantize_saliency: bit-identical
+    const HaarPyramid p = haar_analyze(object, 3);
+    std::vector<double> ref(std::size_t(n) * n * 2);
+    ref_haar_analyze(object.data().data(), n, 3, ref.data());
+    bool same = std::memcmp(p.approx.data().data(), ref.data(), p.approx.size() * 8) == 0;
+    std::size_t o = p.approx.size();
+    for (const auto& b : p.details)
+      for (const RealImage* im : {&b.h, &b.v, &b.d}) {
+        same = same && std::memcmp(im->data().data(), ref.data() + o, im->size() * 8) == 0;
+        o += im->size();
+      }
+    EXPECT(same, "haar_analyze n=%d not bit-identical", n);
+    const SaliencyPyramid sp = quantize_saliency(saliency);
+    ref_quantize_saliency(saliency.data().data(), n, ref.data());
+    same = std::memcmp(sp.by_factor(2).data().data(), ref.data(), std::size_t(n) * n / 4 * 8) == 0 &&
+           std::memcmp(sp.by_factor(4).data().data(), ref.data() + n * n / 4, std::size_t(n) * n / 16 * 8) == 0;
+    EXPECT(same, "quantize_saliency n=%d not bit-identical", n);
+
+    // synthesize_progressive: all four stages, masks, operator counts
+    const SceneParams scene = make_scene(wl, pitch, z, n);
+    const LutSet luts = LutSet::build(scene);
+    const RefinementPlan plan;
+    const ProgressiveResult r = synthesize_progressive(object, saliency, scene, plan, luts);
+    std::vector<double> planes(std::size_t(8) * n * n);
+    std::vector<std::uint8_t> masks(std::size_t(n) * n * 21 / 16);
+    std::uint64_t ops[5];
+    const double th[3] = {plan.t_ll, plan.t_l, plan.t_full};
+    const int en[3] = {1, 1, 1};
+    ref_synthesize_progressive(object.data().data(), saliency.data().data(), n, wl, pitch, z, th, en,
+                               1, 0, 0, planes.data(), masks.data(), ops);
+    for (int s = 0; s < 4; ++s) {
+      const double e = rel_l2(r.stage(s), planes.data() + std::size_t(2) * n * n * s);
+      EXPECT(e <= 1e-4, "synthesize_progressive n=%d stage %d rel L2 %.3e", n, s, e);
+    }
+    EXPECT(std::memcmp(r.mask_ll.on.data(), masks.data(), r.mask_ll.on.size()) == 0, "mask_ll n=%d", n);
+    EXPECT(std::memcmp(r.mask_full.on.data(), masks.data() + n * n / 16 + n * n / 4, r.mask_full.on.size()) == 0,
+           "mask_full n=%d", n);
+    for (int i = 0; i < 5; ++i)
+      EXPECT(r.ops.get(kAllOpLevels[i]) == ops[i], "ops[%d] n=%d: %llu vs %llu", i, n,
+             (unsigned long long)r.ops.get(kAllOpLevels[i]), (unsigned long long)ops[i]);
+
+    // point-wise oracle
+    OpCounter pc;
+    const ComplexField pw = synthesize_pointwise_oracle(object, scene, pc, luts.of(1));
+    std::uint64_t pops = 0;
+    ref_synthesize_pointwise_oracle(object.data().data(), n, wl, pitch, z, 1, planes.data(), &pops);
+    EXPECT(rel_l2(pw, planes.data()) <= 1e-4, "pointwise oracle n=%d", n);
+    EXPECT(pc.get(OpLevel::kPointwiseOracle) == pops, "pointwise ops n=%d", n);
+
+    // apply_block with a complex weight (synthesis.cpp:37-41)
+    ComplexField plane(n, n);
+    OpCounter ac;
+    apply_block(plane, luts.of(2), GridCell{1, 2}, {0.3, -0.7}, ac, OpLevel::kRefineL);
+    std::vector<double> pl(std::size_t(2) * n * n, 0.0);
+    std::uint64_t aops = 0;
+    ref_apply_block(wl, pitch, z, n, 2, 1, 2, 0.3, -0.7, pl.data(), &aops);
+    EXPECT(rel_l2(plane, pl.data()) <= 1e-5, "apply_block complex weight n=%d", n);
+    EXPECT(ac.get(OpLevel::kRefineL) == 1, "apply_block count");
+  }
+  // validation behaviour (synthesis.cpp:184-202)
+  {
+    const SceneParams scene = make_scene(wl, pitch, z, 16);
+    const LutSet luts = LutSet::build(scene);
+    bool threw = false;
+    try {
+      synthesize_progressive(random_image(8, 1), uniform_saliency(8), scene, RefinementPlan{}, luts);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    EXPECT(threw, "size mismatch must throw ValidationError");
+    threw = false;
+    RealImage bad(16, 16);
+    bad.at(1, 1) = 1.5;
+    try {
+      quantize_saliency(bad);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    EXPECT(threw, "saliency out of range must throw ValidationError");
+  }
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
+  return failures ? 1 : 0;
+}
