@@ -5,7 +5,7 @@
  * its "operator API" is the set of C++ free functions listed beside each
  * entry point below. Those functions keep their names, argument meaning and
  * error behaviour in the host mirrors above this ABI (Python:
- * paper_2211_09938_b200/wavecgh.py; C++: include/wavecgh_b200.hpp) and call
+ * paper_2211_09938_b200/stages.py, hologram.py; C++: integration/wavecgh_gpu.cpp) and call
  * these entry points, which launch the kernels. There is no CPU fallback: a
  * missing device or a CUDA failure returns WCGH_ERUNTIME.
  *

@@ -67,7 +67,7 @@ struct wcgh_job {
   DevBuf obj, sal, a_eff, seg_counts, seg_offsets, ops, err, points, plane;
   // LUT method
   DevBuf w_stage, stage_planes, lut_scratch, lut_partial;
-  StageCells cells[4];
+  std::vector<std::unique_ptr<StageCells>> cells;  // [layer * 4 + stage]
   std::vector<std::unique_ptr<DevBuf>> luts;  // [layer * 4 + stage], guarded allocations
   std::vector<float2*> lut_base;              // support element (0, 0) in each
   DirectScratch direct;
@@ -558,7 +558,7 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     WCGH_CUDA(cudaMallocHost(&j->h_offsets, sizeof(int64_t) * (L + 1)));
     WCGH_CUDA(cudaMallocHost(&j->h_ops, sizeof(unsigned long long) * WCGH_OP_LEVELS * L));
     WCGH_CUDA(cudaMallocHost(&j->h_err, sizeof(int) * 4));
-    WCGH_CUDA(cudaMallocHost(&j->h_tot, sizeof(int) * 16));
+    WCGH_CUDA(cudaMallocHost(&j->h_tot, sizeof(int) * 3 * 4 * kMaxLayers));
     for (auto& e : j->ev) WCGH_CUDA(cudaEventCreate(&e));
     if (d.method == WCGH_METHOD_DIRECT) {
       j->points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1));
@@ -707,7 +707,6 @@ __global__ void k_sum_stages(const float2* __restrict__ planes, size_t count, in
 void run_job_lut(wcgh_job* j, cudaStream_t s) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
-  require(L == 1, "job (LUT): multi-layer LUT synthesis is not supported yet; use the direct method");
   j->timing.reset();
   WCGH_CUDA(cudaEventRecord(j->ev[0], s));
   run_analysis(j, s, true);
@@ -716,11 +715,15 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   size_t wofs[4];
   wofs[0] = 0;
   for (int st = 1; st < 4; ++st) wofs[st] = wofs[st - 1] + size_t(ms[st - 1]) * ms[st - 1];
-  // column-major nonzero cell lists per stage (K2 for the LUT path)
-  for (int st = 0; st < 4; ++st) {
-    j->stats.total_launches += launch_stage_cells(j->w_stage.as<float>() + wofs[st], ms[st], j->cells[st], s);
-    stage_cells_totals_async(j->cells[st], j->h_tot + 3 * st, s);
-  }
+  // run lists of the nonzero gated cells per (layer, stage) (K2 for the LUT path)
+  while (j->cells.size() < size_t(L) * 4) j->cells.push_back(std::make_unique<StageCells>());
+  for (int l = 0; l < L; ++l)
+    for (int st = 0; st < 4; ++st) {
+      const float* w = j->w_stage.as<float>() + wstage_len(No) * l + wofs[st];
+      StageCells& sc = *j->cells[size_t(l) * 4 + st];
+      j->stats.total_launches += launch_stage_cells(w, ms[st], sc, s);
+      stage_cells_totals_async(sc, j->h_tot + 3 * (l * 4 + st), s);
+    }
   WCGH_CUDA(cudaMemcpyAsync(j->h_ops, j->ops.p, sizeof(unsigned long long) * WCGH_OP_LEVELS * L, cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaMemcpyAsync(j->h_err, j->ops.as<unsigned long long>() + WCGH_OP_LEVELS * L, sizeof(int), cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
@@ -730,16 +733,19 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   const size_t band = size_t(d.rows) * d.plane_size;
   float2* sp = j->stage_planes.as<float2>();
   long long cells = 0;
-  for (int st = 0; st < 4; ++st) {
-    StageCells& sc = j->cells[st];
-    sc.n_runs = j->h_tot[3 * st];
-    sc.n_dense = j->h_tot[3 * st + 1];
-    sc.nnz = j->h_tot[3 * st + 2];
-    j->stats.total_launches += launch_lut_stage(j->lut_base[st], d.plane_size, blocks[st], sc,
-                                                j->off, d.row0, d.rows, sp + band * st,
-                                                j->lut_partial, s, &j->timing);
-    cells += sc.nnz;
-  }
+  // stage planes accumulate over depth layers (multi-depth = per-layer sum)
+  for (int st = 0; st < 4; ++st)
+    for (int l = 0; l < L; ++l) {
+      const int k = l * 4 + st;
+      StageCells& sc = *j->cells[k];
+      sc.n_runs = j->h_tot[3 * k];
+      sc.n_dense = j->h_tot[3 * k + 1];
+      sc.nnz = j->h_tot[3 * k + 2];
+      j->stats.total_launches += launch_lut_stage(j->lut_base[k], d.plane_size, blocks[st], sc,
+                                                  j->off, d.row0, d.rows, sp + band * st,
+                                                  j->lut_partial, s, &j->timing, l > 0);
+      cells += sc.nnz;
+    }
   j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));
   k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(sp, band, 4, j->plane.as<float2>());

@@ -236,7 +236,7 @@ void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t str
 // listed cells with the block-B LUT; object grid offset `off` on the plane.
 int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
                      int rows, float2* out, DevBuf& partial, cudaStream_t stream,
-                     DirectTiming* timing);
+                     DirectTiming* timing, bool accumulate);
 // Dense weight grid convenience: builds the list, reads nnz (synchronizes),
 // superposes.
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,

@@ -373,10 +373,11 @@ void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t s) 
 }
 
 int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
-                     int rows, float2* out, DevBuf& partial, cudaStream_t s, DirectTiming* timing) {
+                     int rows, float2* out, DevBuf& partial, cudaStream_t s, DirectTiming* timing,
+                     bool accumulate) {
   const size_t band = size_t(rows) * nh;
   if (sc.n_runs == 0) {
-    WCGH_CUDA(cudaMemsetAsync(out, 0, band * sizeof(float2), s));
+    if (!accumulate) WCGH_CUDA(cudaMemsetAsync(out, 0, band * sizeof(float2), s));
     return 0;
   }
   // chunk size depends on the stage's step count only (never on the row band)
@@ -405,7 +406,8 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
     }
     WCGH_CHECK_LAUNCH();
     if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
-    k_reduce_partials<<<unsigned((band + 255) / 256), 256, 0, s>>>(part, ng, band, g0 > 0, out);
+    k_reduce_partials<<<unsigned((band + 255) / 256), 256, 0, s>>>(part, ng, band,
+                                                                  accumulate || g0 > 0, out);
     WCGH_CHECK_LAUNCH();
     launches += 2;
   }
@@ -423,7 +425,8 @@ int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m
   sc.n_dense = tot[1];
   sc.nnz = tot[2];
   if (nnz_out) *nnz_out = sc.nnz;
-  return launches + launch_lut_stage(lut, nh, block, sc, off, row0, rows, out, partial, s, nullptr);
+  return launches + launch_lut_stage(lut, nh, block, sc, off, row0, rows, out, partial, s, nullptr,
+                                    false);
 }
 
 }  // namespace wcgh
