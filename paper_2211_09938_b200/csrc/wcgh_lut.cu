@@ -142,7 +142,7 @@ __global__ void k_runs_fill(const float* __restrict__ w, int m, int R, const int
 }
 
 template <int B, int R, int PX, int D, int W>
-__global__ void __launch_bounds__(W * 32, 3)
+__global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
     k_lut_stage(const float2* __restrict__ lut, int nh, const int4* __restrict__ runs,
                 int n_runs, const float* __restrict__ dense, int off, int row0, int rows,
                 int tiles_x, int chunk0, int chunk_steps, float2* __restrict__ out,
@@ -268,22 +268,22 @@ __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, siz
   out[i] = make_float2(float(re), float(im));
 }
 
-constexpr int kW = 4;  // warps per CTA
 constexpr int kMaxChunkSteps = 4096;
 constexpr size_t kPartialBytes = 2ull << 30;
 
-// Register-window shape (R rows x PX columns per thread, D rows of prefetch).
-// Default 8 x 4 x 2; WCGH_LUT_VARIANT="R,PX,D" selects another compiled shape
-// (tuning only; results are identical up to fp32 summation order).
+// Register-window shape: R rows x PX columns per thread, D rows of prefetch,
+// W warps per CTA. Default 8 x 4 x 2 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
+// another compiled shape (tuning only; results equal up to fp32 rounding).
 struct LutVariant {
-  int R, PX, D;
+  int R, PX, D, W;
 };
 LutVariant lut_variant() {
   static const LutVariant v = [] {
-    LutVariant d{8, 4, 2};
+    LutVariant d{8, 4, 2, 4};
     if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
-      int r = 0, px = 0, dd = 0;
-      if (std::sscanf(e, "%d,%d,%d", &r, &px, &dd) == 3) d = LutVariant{r, px, dd};
+      int r = 0, px = 0, dd = 0, w = 4;
+      const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
+      if (got >= 3) d = LutVariant{r, px, dd, w};
     }
     return d;
   }();
@@ -297,12 +297,12 @@ int lut_chunk_target() {
   return t;
 }
 
-template <int B, int R, int PX, int D>
+template <int B, int R, int PX, int D, int W>
 void launch_stage_v(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
                     int tiles_x, dim3 grid, int chunk0, int chunk_steps, float2* out,
                     size_t stride, cudaStream_t s) {
   const size_t smem = sizeof(float) * size_t(chunk_steps + sc.m + 32);
-  k_lut_stage<B, R, PX, D, kW><<<grid, kW * 32, smem, s>>>(
+  k_lut_stage<B, R, PX, D, W><<<grid, W * 32, smem, s>>>(
       lut, nh, sc.runs.as<int4>(), sc.n_runs, sc.dense.as<float>(), off, row0, rows, tiles_x,
       chunk0, chunk_steps, out, stride);
 }
@@ -311,17 +311,17 @@ template <int B>
 void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageCells& sc, int off,
                     int row0, int rows, int tiles_x, dim3 grid, int chunk0, int chunk_steps,
                     float2* out, size_t stride, cudaStream_t s) {
-#define WCGH_V(R_, PX_, D_)                                                                  \
-  if (v.R == R_ && v.PX == PX_ && v.D == D_) {                                               \
-    launch_stage_v<B, R_, PX_, D_>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,     \
-                                   chunk_steps, out, stride, s);                             \
-    return;                                                                                  \
+#define WCGH_V(R_, PX_, D_, W_)                                                             \
+  if (v.R == R_ && v.PX == PX_ && v.D == D_ && v.W == W_) {                                 \
+    launch_stage_v<B, R_, PX_, D_, W_>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0, \
+                                       chunk_steps, out, stride, s);                        \
+    return;                                                                                 \
   }
-  WCGH_V(8, 4, 2)
-  WCGH_V(16, 2, 2)
-  WCGH_V(16, 2, 4)
-  WCGH_V(8, 2, 4)
-  WCGH_V(12, 2, 4)
+  WCGH_V(8, 4, 2, 4)
+  WCGH_V(8, 4, 2, 8)
+  WCGH_V(8, 4, 4, 8)
+  WCGH_V(8, 4, 3, 4)
+  WCGH_V(12, 4, 2, 8)
 #undef WCGH_V
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
 }
@@ -391,7 +391,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
   const int tiles_x = (nh + 32 * v.PX - 1) / (32 * v.PX);
   const int row_warps = (rows + block * v.R - 1) / (block * v.R) * block;
-  const int tiles_y = (row_warps + kW - 1) / kW;
+  const int tiles_y = (row_warps + v.W - 1) / v.W;
   int launches = 0;
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
     const int ng = std::min(group, n_chunks - g0);
