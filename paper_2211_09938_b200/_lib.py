@@ -15,7 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libwcgh.so"
 
 WCGH_OK, WCGH_EVALIDATION, WCGH_ERUNTIME = 0, 1, 2
 U8, F32, F64 = 0, 1, 2
-METHOD_DIRECT, METHOD_LUT = 0, 1
+METHOD_DIRECT, METHOD_LUT, METHOD_FFT = 0, 1, 2
 PHASE_FIXED, PHASE_FP64 = 0, 1
 OP_LEVELS = 5
 

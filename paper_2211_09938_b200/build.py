@@ -15,7 +15,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "wcgh"
 LIB = PKG / "libwcgh.so"
-SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_abi.cu"]
+SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_fft.cu", "wcgh_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             print((BUILD / (Path(src).stem + ".ptxas.log")).read_text())
     tmp = LIB.with_suffix(".so.tmp")
-    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lcufft", "-lrt", "-ldl",
+          "-lpthread", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     tmp.replace(LIB)
     return LIB
 

@@ -72,6 +72,7 @@ struct wcgh_job {
   std::vector<float2*> lut_base;              // support element (0, 0) in each
   DirectScratch direct;
   DirectTiming timing;
+  FftPlan fft;  // FFT method
   // pinned host staging
   int64_t* h_offsets = nullptr;       // n_layers + 1
   unsigned long long* h_ops = nullptr;  // n_layers * 5
@@ -131,7 +132,9 @@ void job_validate(const wcgh_desc& d) {
           "synthesize_progressive: (plane_size - object_size)/2 must be a multiple of 8");
   require(d.row0 >= 0 && d.rows >= 1 && d.row0 + d.rows <= d.plane_size,
           "job: row band outside the plane");
-  require(d.method == WCGH_METHOD_DIRECT || d.method == WCGH_METHOD_LUT, "job: unknown method");
+  require(d.method == WCGH_METHOD_DIRECT || d.method == WCGH_METHOD_LUT ||
+              d.method == WCGH_METHOD_FFT,
+          "job: unknown method");
   require(d.phase_mode == WCGH_PHASE_FIXED || d.phase_mode == WCGH_PHASE_FP64,
           "job: unknown phase mode");
   dtype_size(d.obj_dtype);
@@ -562,6 +565,10 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     for (auto& e : j->ev) WCGH_CUDA(cudaEventCreate(&e));
     if (d.method == WCGH_METHOD_DIRECT) {
       j->points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1));
+    } else if (d.method == WCGH_METHOD_FFT) {
+      // fringe spectra per layer on the 2Nh grid (precompute)
+      fft_prepare(j->fft, d.layers, L, d.plane_size, ctx->stream);
+      sync(ctx->stream);
     } else {
       // LUT method: precompute the four block LUTs per layer (reported
       // separately from synthesis, like the reference's lut_build).
@@ -652,10 +659,12 @@ void run_job_direct(wcgh_job* j, cudaStream_t s) {
   run_analysis(j, s, false);
   const size_t per_layer = size_t(No) * seg_per_row(No);
   const size_t nseg = per_layer * L;
+  const bool fft = d.method == WCGH_METHOD_FFT;
   launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s);
-  launch_compact_points(j->a_eff.as<float>(), j->seg_offsets.as<int>(), No, L, j->off, 0,
-                        j->points.as<wcgh_point>(), s);
-  j->stats.total_launches += 2;
+  if (!fft)
+    launch_compact_points(j->a_eff.as<float>(), j->seg_offsets.as<int>(), No, L, j->off, 0,
+                          j->points.as<wcgh_point>(), s);
+  j->stats.total_launches += fft ? 1 : 2;
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
   // layer boundaries of the compacted list, ops and validation flags
   for (int l = 0; l <= L; ++l) {
@@ -676,9 +685,17 @@ void run_job_direct(wcgh_job* j, cudaStream_t s) {
   const double far = double(j->off + No - 1);
   const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
                                  std::fabs(double(d.row0 + d.rows - 1) - j->off));
-  const int launches = launch_direct(j->points.as<wcgh_point>(), lb, L, d.layers, d.plane_size,
-                                     d.row0, d.rows, d.phase_mode, far, max_dy,
-                                     j->plane.as<float2>(), j->direct, s, &j->timing, &j->stats.updates);
+  int launches = 0;
+  if (fft) {
+    // same hologram by FFT correlation; `updates` keeps the direct-sum count
+    j->stats.updates = double(lb[L]) * double(d.rows) * double(d.plane_size);
+    launches = launch_fft_synthesis(j->fft, j->a_eff.as<float>(), No, j->off, d.plane_size,
+                                    d.row0, d.rows, j->plane.as<float2>(), s, &j->timing);
+  } else {
+    launches = launch_direct(j->points.as<wcgh_point>(), lb, L, d.layers, d.plane_size, d.row0,
+                             d.rows, d.phase_mode, far, max_dy, j->plane.as<float2>(), j->direct,
+                             s, &j->timing, &j->stats.updates);
+  }
   j->stats.synth_launches = j->timing.launches();
   j->stats.total_launches += launches;
   WCGH_CUDA(cudaEventRecord(j->ev[3], s));
@@ -774,10 +791,10 @@ int wcgh_job_run(wcgh_job* job) {
     require(job->uploaded, "job_run: inputs not uploaded");
     use_device(job->ctx);
     job->stats = wcgh_stats{};
-    if (job->desc.method == WCGH_METHOD_DIRECT)
-      run_job_direct(job, job->ctx->stream);
-    else
+    if (job->desc.method == WCGH_METHOD_LUT)
       run_job_lut(job, job->ctx->stream);
+    else  // direct and FFT share the analysis + compaction front end
+      run_job_direct(job, job->ctx->stream);
   });
 }
 

@@ -200,6 +200,23 @@ int launch_expand_residual(const double* h, const double* v, const double* d, in
 
 // ---- LUT path (K4 + K5) ------------------------------------------------------
 
+// ---- FFT-convolution method ---------------------------------------------------
+
+struct FftPlan {
+  int L = 0, n_layers = 0;
+  int plan = 0;  // cufftHandle
+  DevBuf fringe_spec, grid, acc;
+  FftPlan() = default;
+  FftPlan(const FftPlan&) = delete;
+  FftPlan& operator=(const FftPlan&) = delete;
+  ~FftPlan();
+};
+// Per-layer fringe spectra on the 2Nh x 2Nh grid (precompute).
+void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cudaStream_t stream);
+// out (rows x nh) = band of sum_layers A_eff_l (*) F_l.
+int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
+                         int rows, float2* out, cudaStream_t stream, DirectTiming* timing);
+
 // LUT supports live in guarded allocations: kLutGuardRows zeroed rows before
 // and after the (2n-1)^2 support plus kLutPadCols zeroed tail elements, so
 // the superposition kernel's register window never needs bounds checks.

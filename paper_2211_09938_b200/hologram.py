@@ -24,7 +24,7 @@ class JobSpec:
     enable_ll: bool = True
     enable_l: bool = True
     enable_full: bool = True
-    method: str = "direct"        # "direct" | "lut"
+    method: str = "direct"        # "direct" | "lut" | "fft"
     phase: str = "fixed"          # "fixed" | "fp64"
     row0: int = 0
     rows: int | None = None
@@ -50,9 +50,10 @@ class HologramJob:
         d.layers = C.cast(self._layers, C.POINTER(L.Layer))
         d.plan = L.Plan(spec.t_ll, spec.t_l, spec.t_full, int(spec.enable_ll),
                         int(spec.enable_l), int(spec.enable_full))
-        d.method = L.METHOD_DIRECT if spec.method == "direct" else L.METHOD_LUT
-        if spec.method not in ("direct", "lut"):
+        methods = {"direct": L.METHOD_DIRECT, "lut": L.METHOD_LUT, "fft": L.METHOD_FFT}
+        if spec.method not in methods:
             raise L.ValidationError(f"unknown method {spec.method!r}")
+        d.method = methods[spec.method]
         d.phase_mode = L.PHASE_FIXED if spec.phase == "fixed" else L.PHASE_FP64
         d.row0 = spec.row0
         d.rows = self.rows
