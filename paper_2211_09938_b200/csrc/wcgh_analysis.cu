@@ -200,10 +200,11 @@ __global__ void __launch_bounds__(256) k_analysis(const TO* __restrict__ obj, do
       float* w_l = w_ll + size_t(m2) * m2;
       float* w_f = w_l + size_t(m1) * m1;
       w_l[size_t(qy) * m1 + qx] = g_l ? float(r_l) : 0.0f;
-      *reinterpret_cast<float2*>(w_f + r0) =
-          make_float2(gf00 ? float(rf00) : 0.0f, gf01 ? float(rf01) : 0.0f);
-      *reinterpret_cast<float2*>(w_f + r0 + n) =
-          make_float2(gf10 ? float(rf10) : 0.0f, gf11 ? float(rf11) : 0.0f);
+      // scalar stores: w_f's offset is odd when n/8 is odd (no float2 alignment)
+      w_f[r0] = gf00 ? float(rf00) : 0.0f;
+      w_f[r0 + 1] = gf01 ? float(rf01) : 0.0f;
+      w_f[r0 + n] = gf10 ? float(rf10) : 0.0f;
+      w_f[r0 + n + 1] = gf11 ? float(rf11) : 0.0f;
       if (lead2) w_ll[size_t(qy2) * m2 + qx2] = g_ll ? float(r_ll) : 0.0f;
       if (lead3) w_base[size_t(qy3) * m3 + qx3] = float(q3.a);
     }
