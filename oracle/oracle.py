@@ -384,3 +384,48 @@ def ref_ssim(a, b, window=8, k1=0.01, k2=0.03, dynamic_range=1.0):
 
 def ref_default_workers() -> int:
     return int(ref().ref_default_worker_count())
+
+
+# ---- full-plane fp64 oracle by FFT (for the 4096^2 configs) -------------------
+
+def fft_hologram(a_eff_layers, layers, plane_size: int, rows: tuple[int, int] | None = None):
+    """fp64 H = sum_layers A_eff (*) F on a 2Nh circular grid (no wrap reaches
+    the output window since 2Nh >= Nh + No - 1), F the exact point fringe
+    (fringe_lut.cpp:27-32). Mathematically the direct sum of
+    tests/support/oracles.cpp:12-36; pinned against it and against the
+    reference's goldens in tests/test_oracle_pins.py. Multi-threaded scipy FFT."""
+    import scipy.fft as sf
+
+    a = np.asarray(a_eff_layers, np.float64)
+    if a.ndim == 2:
+        a = a[None]
+    nl, no, _ = a.shape
+    n = plane_size
+    L = 2 * n
+    off = (n - no) // 2
+    c = np.arange(L)
+    d = np.where(c < n, c, c - L).astype(np.float64)
+    acc = None
+    for l in range(nl):
+        wl, pitch, z = layers[l]
+        k = 2.0 * np.pi / wl
+        px = (d * pitch)[None, :]
+        py = (d * pitch)[:, None]
+        r = np.sqrt(px * px + py * py + z * z)
+        f = np.exp(1j * k * r) / r
+        f[n, :] = 0.0
+        f[:, n] = 0.0
+        g = np.zeros((L, L), np.complex128)
+        g[off:off + no, off:off + no] = a[l]
+        spec = sf.fft2(g, workers=-1) * sf.fft2(f, workers=-1)
+        acc = spec if acc is None else acc + spec
+        del f, g
+    h = sf.ifft2(acc, workers=-1)
+    r0, r1 = (0, n) if rows is None else rows
+    return np.ascontiguousarray(h[r0:r1, :n])
+
+
+def scene_a_eff(objects: np.ndarray, saliency01: np.ndarray, t=(0.5, 0.7, 0.9), en=(1, 1, 1)):
+    """Per-layer fp64 A_eff of a layered scene (orc_analysis)."""
+    return np.stack([analysis(objects[l], saliency01[l], t, en)["a_eff"]
+                     for l in range(objects.shape[0])])

@@ -1,0 +1,42 @@
+"""Full-plane parity at the 4096^2 configs (BASELINE.json configs[3], [4]):
+every method's whole hologram against the fp64 FFT oracle (oracle.fft_hologram,
+pinned to the reference and to the direct Eq.(1) oracle in
+test_oracle_pins.py): relative L2 <= 1e-4 over all 16.8 M pixels and SSIM
+>= 0.999 between angular-spectrum reconstructions (angular_spectrum.cpp:46-61,
+metrics.cpp:50-85, dynamic range of the reference reconstruction)."""
+import functools
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2211_09938_b200 import scenes
+from paper_2211_09938_b200.hologram import HologramJob, spec_for_scene
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-4
+
+
+@functools.lru_cache(maxsize=2)
+def _oracle(cfg):
+    sc = scenes.make_scene(cfg)
+    c = sc.config
+    a = O.scene_a_eff(sc.objects.astype(np.float64), sc.masks * (1.0 / 255.0))
+    h = O.fft_hologram(a, [(c.wavelength, c.pitch, z) for z in c.depths], c.plane_size)
+    # reconstruct at the first layer's depth (the reference's metrics use the scene z)
+    r = O.reconstruct(h, c.wavelength, c.pitch, c.depths[0])
+    return sc, h, r
+
+
+@pytest.mark.parametrize("cfg", [4, 3])
+@pytest.mark.parametrize("method", ["fft", "lut", "direct"])
+def test_full_plane_4096(ctx, cfg, method):
+    sc, ref, ref_rec = _oracle(cfg)
+    c = sc.config
+    holo = HologramJob(spec_for_scene(sc, method=method))(sc.objects, sc.masks)
+    err = O.rel_l2(holo, ref)
+    assert err <= REL_L2, err
+    rec = O.reconstruct(holo, c.wavelength, c.pitch, c.depths[0])
+    s = O.ssim(rec, ref_rec, 8, 0.01, 0.03, float(ref_rec.max() - ref_rec.min()))
+    assert s >= 0.999, s

@@ -126,3 +126,29 @@ def test_oracle_matches_reference_library_live():
     assert np.abs(r1 - r2).max() <= 1e-12 * np.abs(r2).max()
     dr = r2.max() - r2.min()
     assert abs(O.ssim(r1, r2 * 0.97, 8, 0.01, 0.03, dr) - O.ref_ssim(r1, r2 * 0.97, 8, 0.01, 0.03, dr)) < 1e-12
+
+
+def test_fft_oracle_matches_reference_and_direct_sum():
+    # the full-plane fp64 FFT oracle reproduces the reference's own outputs...
+    g = golden("ref_cfg0")
+    an = O.analysis(g["object"].astype(np.float64), g["mask"] * (1.0 / 255.0))
+    h = O.fft_hologram(an["a_eff"], [(WL, 8e-6, 0.2)], 128)
+    assert O.max_rel_error(h, g["after_full"]) <= 1e-10
+    g = golden("ref_padded_32on64")
+    a = O.analysis(g["object"].astype(np.float64), g["mask"] * (1.0 / 255.0))["a_eff"]
+    assert O.max_rel_error(O.fft_hologram(a, [(WL, 8e-6, 0.05)], 64), g["after_full"]) <= 1e-10
+    g = golden("ref_two_layers_64")
+    a = O.scene_a_eff(g["objects"], g["saliency"])
+    h = O.fft_hologram(a, [(WL, 8e-6, z) for z in g["depths"]], 64)
+    assert O.max_rel_error(h, g["after_full"]) <= 1e-10
+    # ...and the direct Eq.(1) oracle on an object smaller than the plane
+    from paper_2211_09938_b200 import scenes
+
+    sc = scenes.make_scene(scenes.SceneConfig("t", 0, 64, 256, 8e-6, (0.2,)))
+    a = O.scene_a_eff(sc.objects.astype(np.float64), sc.masks / 255.0)
+    h = O.fft_hologram(a, [(WL, 8e-6, 0.2)], 256)
+    xs, ys, amps, lay = O.compact(a[0], off=96)
+    rng = np.random.default_rng(2)
+    px, py = rng.integers(0, 256, 300), rng.integers(0, 256, 300)
+    ref = O.direct_pixels(xs, ys, amps, lay, [(WL, 8e-6, 0.2)], px, py)
+    assert O.max_rel_error(h[py, px], ref) <= 1e-10
