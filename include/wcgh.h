@@ -220,6 +220,21 @@ int wcgh_job_download_stages(wcgh_job* job, float* out4);
 void* wcgh_job_plane_dev(wcgh_job* job);
 int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out);
 
+/* ---- CGH1 hologram files (image_io.cpp:220-278) --------------
+ * "CGH1", u16 version = 1, u32 N, f64 wavelength, f64 pitch, f64 z (little
+ * endian, 34 bytes), then N^2 interleaved f32 (re, im), row-major — exactly
+ * the device complex64 layout. Host I/O; no device needed. File errors return
+ * WCGH_ERUNTIME (IoError); a bad scene or non-finite payload WCGH_EVALIDATION. */
+int wcgh_write_cgh1(const char* path, const float* plane, int n, const wcgh_layer* scene);
+/* Reads a CGH1 file: header into *n_out / *scene_out (either may be NULL),
+ * payload into `plane` if it is non-NULL and capacity >= N^2 complex64. */
+int wcgh_read_cgh1(const char* path, float* plane, int64_t capacity, int* n_out,
+                   wcgh_layer* scene_out);
+/* Writes the last run's full plane (stage < 0) or a LUT-method stage
+ * snapshot (0..3 = base_LLL, after_LL, after_L, after_full) of a whole-plane
+ * job (row0 = 0, rows = plane_size) as CGH1, scene = layer 0. */
+int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage);
+
 /* One-shot: job create + upload + run + download + destroy. The entry the
  * C++ synthesize_progressive mirror calls (synthesis.hpp:88-91). */
 int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object,

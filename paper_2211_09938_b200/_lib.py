@@ -87,6 +87,9 @@ _SIGS = [
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),
     ("wcgh_job_plane_dev", _VP, [_VP]),
     ("wcgh_job_stats", C.c_int, [_VP, C.POINTER(Stats)]),
+    ("wcgh_write_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int, C.POINTER(Layer)]),
+    ("wcgh_read_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int64, C.POINTER(C.c_int), C.POINTER(Layer)]),
+    ("wcgh_job_write_cgh1", C.c_int, [_VP, C.c_char_p, C.c_int]),
     ("wcgh_synthesize", C.c_int, [_VP, C.POINTER(Desc), _VP, _VP, _VP, C.POINTER(Stats)]),
 ]
 EXPORTED = [s[0] for s in _SIGS]

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -834,6 +835,93 @@ int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out) {
   return guard(job ? job->ctx : nullptr, [&] {
     require(job && out, "job_stats: NULL argument");
     *out = job->stats;
+  });
+}
+
+// ---- CGH1 files (image_io.cpp:220-278): 34-byte header + f32 payload ------
+
+int wcgh_write_cgh1(const char* path, const float* plane, int n, const wcgh_layer* scene) {
+  return guard(nullptr, [&] {
+    require(path && plane && scene, "save_hologram: NULL argument");
+    validate_layer(*scene);
+    require(is_pow2(n), "save_hologram: field size does not match scene plane_size");
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw RuntimeError(std::string("hologram: cannot open ") + path + " for writing");
+    const char magic[4] = {'C', 'G', 'H', '1'};
+    const uint16_t version = 1;
+    const uint32_t un = uint32_t(n);
+    bool ok = std::fwrite(magic, 1, 4, f) == 4 && std::fwrite(&version, 2, 1, f) == 1 &&
+              std::fwrite(&un, 4, 1, f) == 1 && std::fwrite(&scene->wavelength, 8, 1, f) == 1 &&
+              std::fwrite(&scene->pitch, 8, 1, f) == 1 && std::fwrite(&scene->z, 8, 1, f) == 1;
+    const size_t count = size_t(n) * n * 2;
+    ok = ok && std::fwrite(plane, sizeof(float), count, f) == count;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw RuntimeError(std::string("hologram: write failed for ") + path);
+  });
+}
+
+int wcgh_read_cgh1(const char* path, float* plane, int64_t capacity, int* n_out,
+                   wcgh_layer* scene_out) {
+  return guard(nullptr, [&] {
+    require(path != nullptr, "load_hologram: NULL path");
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw RuntimeError(std::string("hologram: cannot open ") + path);
+    struct Closer {
+      std::FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "CGH1", 4) != 0)
+      throw RuntimeError(std::string("hologram: bad magic in ") + path);
+    uint16_t version = 0;
+    uint32_t un = 0;
+    wcgh_layer sc{};
+    if (std::fread(&version, 2, 1, f) != 1 || std::fread(&un, 4, 1, f) != 1 ||
+        std::fread(&sc.wavelength, 8, 1, f) != 1 || std::fread(&sc.pitch, 8, 1, f) != 1 ||
+        std::fread(&sc.z, 8, 1, f) != 1)
+      throw RuntimeError("hologram: truncated or unreadable header");
+    if (version != 1) throw RuntimeError("hologram: unsupported version " + std::to_string(version));
+    validate_layer(sc);
+    require(un > 0 && un <= 65536 && is_pow2(int(un)),
+            "scene: plane_size must be a power of two, got " + std::to_string(un));
+    if (n_out) *n_out = int(un);
+    if (scene_out) *scene_out = sc;
+    if (plane) {
+      const size_t count = size_t(un) * un;
+      require(capacity >= int64_t(count), "load_hologram: output buffer too small");
+      if (std::fread(plane, sizeof(float) * 2, count, f) != count)
+        throw RuntimeError("hologram: truncated payload");
+      for (size_t i = 0; i < 2 * count; ++i)
+        if (!std::isfinite(plane[i]))
+          throw ValidationError(std::string("hologram ") + path + ": non-finite sample");
+    }
+  });
+}
+
+int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && path, "job_write_cgh1: NULL argument");
+    const wcgh_desc& d = job->desc;
+    require(d.row0 == 0 && d.rows == d.plane_size,
+            "save_hologram: field size does not match scene plane_size (job holds a row band)");
+    require(stage < 4, "job_write_cgh1: stage index out of range");
+    const size_t count = size_t(d.plane_size) * d.plane_size;
+    std::vector<float> host(2 * count);
+    if (stage < 0) {
+      use_device(job->ctx);
+      WCGH_CUDA(cudaMemcpyAsync(host.data(), job->plane.p, sizeof(float2) * count, cudaMemcpyDeviceToHost,
+                                job->ctx->stream));
+      sync(job->ctx->stream);
+    } else {
+      std::vector<float> all(8 * count);
+      const int rc = wcgh_job_download_stages(job, all.data());
+      if (rc == WCGH_EVALIDATION) throw ValidationError(t_last_error);
+      if (rc) throw RuntimeError(t_last_error);
+      std::memcpy(host.data(), all.data() + 2 * count * size_t(stage), sizeof(float) * 2 * count);
+    }
+    const int rc = wcgh_write_cgh1(path, host.data(), d.plane_size, &job->layers[0]);
+    if (rc == WCGH_EVALIDATION) throw ValidationError(t_last_error);
+    if (rc) throw RuntimeError(t_last_error);
   });
 }
 

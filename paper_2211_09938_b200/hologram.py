@@ -135,3 +135,8 @@ def spec_for_scene(scene, method: str | None = None, phase: str = "fixed", row0:
     return JobSpec(object_size=c.object_size, plane_size=c.plane_size,
                    layers=[(c.wavelength, c.pitch, z) for z in c.depths],
                    method=method or c.method, phase=phase, row0=row0, rows=rows, **plan)
+
+
+def write_job_cgh1(job: HologramJob, path, stage: int = -1) -> None:
+    """The job's last plane (stage < 0) or LUT stage snapshot as a CGH1 file."""
+    L.check(job.ctx.lib.wcgh_job_write_cgh1(job.h, str(path).encode(), int(stage)))

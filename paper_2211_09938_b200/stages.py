@@ -152,3 +152,24 @@ def refine(plane: np.ndarray, layer, h, v, d, saliency_finer, threshold: float, 
     L.check(c.lib.wcgh_refine(c.h, C.byref(lay), n, L.ptr(h), L.ptr(v), L.ptr(d), m, L.ptr(sal),
                               float(threshold), L.ptr(plane), L.ptr(mask), C.byref(ops)))
     return mask, int(ops.value)
+
+
+def write_cgh1(path, plane: np.ndarray, layer) -> None:
+    """save_hologram (image_io.cpp:220-242): CGH1 header + f32 (re, im) payload."""
+    plane = np.ascontiguousarray(plane, np.complex64)
+    n = plane.shape[0]
+    if plane.ndim != 2 or plane.shape[1] != n:
+        raise L.ValidationError("save_hologram: field size does not match scene plane_size")
+    lay = L.Layer(*layer)
+    L.check(L.load().wcgh_write_cgh1(str(path).encode(), L.ptr(plane), n, C.byref(lay)))
+
+
+def read_cgh1(path):
+    """load_hologram (image_io.cpp:244-278) -> (plane complex64, (wavelength, pitch, z))."""
+    lib = L.load()
+    n = C.c_int(0)
+    lay = L.Layer()
+    L.check(lib.wcgh_read_cgh1(str(path).encode(), None, 0, C.byref(n), C.byref(lay)))
+    plane = np.empty((n.value, n.value), np.complex64)
+    L.check(lib.wcgh_read_cgh1(str(path).encode(), L.ptr(plane), plane.size, C.byref(n), C.byref(lay)))
+    return plane, (lay.wavelength, lay.pitch, lay.z)
