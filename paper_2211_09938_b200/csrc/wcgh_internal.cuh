@@ -217,20 +217,23 @@ void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cu
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
                          int rows, float2* out, cudaStream_t stream, DirectTiming* timing);
 
-// LUT supports live in guarded allocations: kLutGuardRows zeroed rows before
-// and after the (2n-1)^2 support plus kLutPadCols zeroed tail elements, so
-// the superposition kernel's register window never needs bounds checks.
-constexpr int kLutGuardRows = 96;
+// LUT supports live in guarded allocations: zeroed guard rows before
+// (prefetch below row 0: <= B*(D+1)+1 rows) and after (a CTA's last row
+// groups overhang the band by < B*R*W rows; they compute on guard data and are
+// never stored) plus kLutPadCols zeroed tail elements, so the superposition
+// kernel's register window never needs bounds checks.
+constexpr int kLutGuardBefore = 64;
+constexpr int kLutGuardAfter = 8 * 8 * 4 + 16;  // B*R*W for the compiled W = 4 shapes
 constexpr int kLutPadCols = 256;
 inline size_t lut_alloc_bytes(int n) {
   const size_t span = size_t(2 * n - 1);
-  return ((span + 2 * kLutGuardRows) * span + kLutPadCols) * sizeof(float2);
+  return ((span + kLutGuardBefore + kLutGuardAfter) * span + kLutPadCols) * sizeof(float2);
 }
 // Zeroes the allocation and returns the pointer to support element (0, 0).
 inline float2* lut_in_alloc(DevBuf& buf, int n, cudaStream_t s) {
   buf.reserve(lut_alloc_bytes(n));
   WCGH_CUDA(cudaMemsetAsync(buf.p, 0, lut_alloc_bytes(n), s));
-  return buf.as<float2>() + size_t(kLutGuardRows) * size_t(2 * n - 1);
+  return buf.as<float2>() + size_t(kLutGuardBefore) * size_t(2 * n - 1);
 }
 
 // Builds the (2n-1)^2 complex64 support of block size B (fp64 sums).

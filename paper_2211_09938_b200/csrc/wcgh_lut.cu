@@ -151,8 +151,12 @@ __global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
   constexpr int S = R + D;  // ring: R live diagonals + D prefetched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = blockIdx.x % tiles_x, tyc = blockIdx.x / tiles_x;
-  const int rw = tyc * W + warp;          // row-warp: R rows at stride B
-  const int yb = (rw / B) * (B * R) + rw % B;  // band row of pixel row 0
+  // The W warps of a CTA share one row residue r (mod B) and take consecutive
+  // row groups (R rows at stride B each), so the LUT rows one warp loads are
+  // the rows the next warp needs R steps later (L1 reuse at every B).
+  const int r = tyc % B;
+  const int g = (tyc / B) * W + warp;
+  const int yb = g * (B * R) + r;  // band row of pixel row 0
   const int x0 = tx * (32 * PX) + lane;
   const int span = 2 * nh - 1;
   const int d_lo = (chunk0 + blockIdx.y) * chunk_steps;
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
     for (int i = 0; i < PX; ++i) acc[j][i] = make_float2(0.f, 0.f);
 
   // LUT row of pixel row j at cell row cy: (row0 + yb + jB) - off - B cy + nh - 1.
-  // `lut` points into a guarded allocation (kLutGuardRows rows before and
+  // `lut` points into a guarded allocation (guard rows before and
   // after, kLutPadCols elements of tail padding), so the window and the
   // prefetch never need clamping; out-of-plane pixels read guard data and
   // are never stored.
@@ -318,10 +322,8 @@ void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageC
     return;                                                                                 \
   }
   WCGH_V(8, 4, 2, 4)
-  WCGH_V(8, 4, 2, 8)
-  WCGH_V(8, 4, 4, 8)
   WCGH_V(8, 4, 3, 4)
-  WCGH_V(12, 4, 2, 8)
+  WCGH_V(8, 2, 4, 4)
 #undef WCGH_V
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
 }
@@ -383,6 +385,8 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   // chunk size depends on the stage's step count only (never on the row band)
   const LutVariant v = lut_variant();
   require(sc.gap == v.R, "LUT superposition: run lists built for another window height");
+  require(block * v.R * v.W <= kLutGuardAfter - 16 && block * (v.D + 1) + 1 <= kLutGuardBefore,
+          "LUT superposition: window shape exceeds the LUT guard rows");
   const int target = lut_chunk_target();
   int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + target - 1) / target));
   chunk_steps = (chunk_steps + 127) / 128 * 128;
@@ -390,8 +394,8 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
   float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
   const int tiles_x = (nh + 32 * v.PX - 1) / (32 * v.PX);
-  const int row_warps = (rows + block * v.R - 1) / (block * v.R) * block;
-  const int tiles_y = (row_warps + v.W - 1) / v.W;
+  const int groups = (rows + block * v.R - 1) / (block * v.R);  // per row residue
+  const int tiles_y = block * ((groups + v.W - 1) / v.W);
   int launches = 0;
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
     const int ng = std::min(group, n_chunks - g0);
