@@ -223,7 +223,7 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
 // never stored) plus kLutPadCols zeroed tail elements, so the superposition
 // kernel's register window never needs bounds checks.
 constexpr int kLutGuardBefore = 64;
-constexpr int kLutGuardAfter = 8 * 8 * 4 + 16;  // B*R*W for the compiled W = 4 shapes
+constexpr int kLutGuardAfter = 8 * 8 * 8 + 16;  // B*R*W for the compiled shapes (W <= 8)
 constexpr int kLutPadCols = 256;
 inline size_t lut_alloc_bytes(int n) {
   const size_t span = size_t(2 * n - 1);

@@ -141,8 +141,28 @@ __global__ void k_runs_fill(const float* __restrict__ w, int m, int R, const int
   if (cur >= 0 && lane == 0) runs[cur].z = last - start + 1;
 }
 
+// acc + w * v on both lanes of a complex sample: one packed FFMA2
+// (fma.rn.f32x2, sm_100a) -- per lane the same IEEE fma as fmaf, so results
+// are bit-identical to the scalar form at half the issued instructions.
+__device__ __forceinline__ float2 ffma2(float w, float2 v, float2 a) {
+  float2 r;
+  asm("{\n .reg .b64 pv, pw, pa, pr;\n mov.b64 pv, {%2, %3};\n mov.b64 pw, {%4, %4};\n"
+      " mov.b64 pa, {%5, %6};\n fma.rn.f32x2 pr, pw, pv, pa;\n mov.b64 {%0, %1}, pr;\n}\n"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(v.x), "f"(v.y), "f"(w), "f"(a.x), "f"(a.y));
+  return r;
+}
+
+// Resident CTAs per SM the register budget is sized for: accumulators
+// (2 R PX) + ring (2 (R + D) PX) + ~24 for addressing, per thread.
+constexpr int lut_min_blocks(int R, int PX, int D, int W) {
+  return 65536 / (W * 32 * (4 * R * PX + 2 * D * PX + 24)) > 0
+             ? 65536 / (W * 32 * (4 * R * PX + 2 * D * PX + 24))
+             : 1;
+}
+
 template <int B, int R, int PX, int D, int W>
-__global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
+__global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
     k_lut_stage(const float2* __restrict__ lut, int nh, const int4* __restrict__ runs,
                 int n_runs, const float* __restrict__ dense, int off, int row0, int rows,
                 int tiles_x, int chunk0, int chunk_steps, float2* __restrict__ out,
@@ -194,8 +214,10 @@ __global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
   // are never stored.
   const int rho_base = row0 + yb - off + nh - 1;
   const long long row_step = (long long)B * span;  // one cell row down the LUT
+  int4 next = r_lo < r_hi ? __ldg(runs + r_lo) : make_int4(0, 0, 0, 0);
   for (int ri = r_lo; ri < r_hi; ++ri) {
-    const int4 run = __ldg(runs + ri);  // (c_x, c_y start, steps, dense offset)
+    const int4 run = next;  // (c_x, c_y start, steps, dense offset)
+    if (ri + 1 < r_hi) next = __ldg(runs + ri + 1);  // one run ahead
     const int cx = run.x, cy_s = run.y, n_steps = run.z;
     const float* ws = s_w + (run.w - w_lo);
     const float2* rp = lut + (x0 - off - B * cx + nh - 1) + (long long)(rho_base - B * cy_s) * span;
@@ -219,9 +241,7 @@ __global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
     if (wv != 0.f) {                                                            \
       _Pragma("unroll") for (int j = 0; j < R; ++j)                             \
       _Pragma("unroll") for (int i = 0; i < PX; ++i) {                          \
-        const float2 v = ring[(j - (uu) + 2 * S) % S][i];                       \
-        acc[j][i].x = fmaf(wv, v.x, acc[j][i].x);                               \
-        acc[j][i].y = fmaf(wv, v.y, acc[j][i].y);                               \
+        acc[j][i] = ffma2(wv, ring[(j - (uu) + 2 * S) % S][i], acc[j][i]);      \
       }                                                                         \
     }                                                                           \
     _Pragma("unroll") for (int i = 0; i < PX; ++i)                              \
@@ -239,6 +259,154 @@ __global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
     }
 #undef WCGH_LUT_STEP
   }
+
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int row = yb + j * B;
+    if (row < rows) {
+      float2* dst = out + size_t(blockIdx.y) * out_stride + size_t(row) * nh;
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        const int x = x0 + 32 * i;
+        if (x < nh) dst[x] = acc[j][i];
+      }
+    }
+  }
+}
+
+// ---- K4b: same tile walk, LUT rows staged through a per-warp shared-memory
+// ring by cp.async R steps ahead (latency hidden by the async copy instead
+// of by registers). Per step a thread issues PX 8-byte cp.async for the row
+// needed R+1 steps later and PX LDS for the row needed next step; the MAC
+// reads registers only. The register ring has R+1 slots and the smem ring
+// R+1 slots, so every ring index is a compile-time constant inside the
+// (R+1)-step unrolled body. Each thread reads back only what it copied, so
+// no cross-thread barrier is needed; cp.async.wait_group(R-1) before each
+// LDS is the only synchronisation.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(dst),
+      "l"(src), "r"(int(pred))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int B, int R, int PX, int W>
+__global__ void __launch_bounds__(W * 32, (W <= 4) ? 3 : 1)
+    k_lut_stage_cp(const float2* __restrict__ lut, int nh, const int4* __restrict__ runs,
+                   int n_runs, const float* __restrict__ dense, int off, int row0, int rows,
+                   int tiles_x, int chunk0, int chunk_steps, float2* __restrict__ out,
+                   size_t out_stride) {
+  constexpr int S = R + 1;  // ring period (registers and shared memory)
+  extern __shared__ float4 s_dyn[];
+  float2* s_ring = reinterpret_cast<float2*>(s_dyn);              // W x S x (32 PX)
+  float* s_w = reinterpret_cast<float*>(s_ring + W * S * 32 * PX);  // step weights
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = blockIdx.x % tiles_x, tyc = blockIdx.x / tiles_x;
+  const int r = tyc % B;
+  const int g = (tyc / B) * W + warp;
+  const int yb = g * (B * R) + r;
+  const int x0 = tx * (32 * PX) + lane;
+  const int span = 2 * nh - 1;
+  const int d_lo = (chunk0 + blockIdx.y) * chunk_steps;
+  const int d_hi = d_lo + chunk_steps;
+
+  auto lower_bound = [&](int key) {
+    int lo = 0, hi = n_runs;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(&runs[mid].w) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const int r_lo = lower_bound(d_lo), r_hi = lower_bound(d_hi);
+  int w_lo = 0;
+  if (r_lo < r_hi) {
+    w_lo = __ldg(&runs[r_lo].w);
+    const int4 lr = __ldg(runs + r_hi - 1);
+    const int w_n = lr.w + lr.z - w_lo;
+    for (int i = threadIdx.x; i < w_n; i += W * 32) s_w[i] = __ldg(dense + w_lo + i);
+  }
+  __syncthreads();
+
+  float2 acc[R][PX];
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int i = 0; i < PX; ++i) acc[j][i] = make_float2(0.f, 0.f);
+
+  float2* my_ring = s_ring + warp * (S * 32 * PX) + lane;  // slot k, column i: [k*32PX + 32i]
+  const unsigned ring_sa = smem_addr(my_ring);
+  const int rho_base = row0 + yb - off + nh - 1;
+  const long long row_step = (long long)B * span;
+  for (int ri = r_lo; ri < r_hi; ++ri) {
+    const int4 run = __ldg(runs + ri);
+    const int cx = run.x, cy_s = run.y, n_steps = run.z;
+    const float* ws = s_w + (run.w - w_lo);
+    const float2* rp = lut + (x0 - off - B * cx + nh - 1) + (long long)(rho_base - B * cy_s) * span;
+    // register slot (t mod S) holds diagonal t; diagonals 0..R-1 come straight from L2
+    float2 reg[S][PX];
+    {
+      const float2* rt = rp;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+#pragma unroll
+        for (int i = 0; i < PX; ++i) reg[t][i] = __ldg(rt + 32 * i);
+        rt += row_step;
+      }
+    }
+    // shared slot (n mod S) holds diagonal -n; diagonal -n is needed at step n
+#pragma unroll
+    for (int n = 1; n <= R; ++n) {
+      const float2* src = rp - n * row_step;
+#pragma unroll
+      for (int i = 0; i < PX; ++i)
+        cp_async8(ring_sa + unsigned(((n % S) * 32 * PX + 32 * i) * sizeof(float2)), src + 32 * i,
+                  n < n_steps);
+      cp_async_commit();
+    }
+    const float2* pf = rp - (R + 1) * row_step;  // next diagonal to stage: -(R+1)
+    // step u (uu = u mod S): stage-in diagonal -(u+1) to registers, MAC, then
+    // refill shared slot uu (diagonal -u, consumed) with diagonal -(u+1+R)
+#define WCGH_LUT_CP_STEP(uu, u)                                                        \
+  {                                                                                    \
+    cp_async_wait<R - 1>();                                                            \
+    if ((u) + 1 < n_steps) {                                                           \
+      _Pragma("unroll") for (int i = 0; i < PX; ++i)                                   \
+        reg[(R - (uu)) % S][i] = my_ring[(((uu) + 1) % S) * 32 * PX + 32 * i];         \
+    }                                                                                  \
+    const float wv = ws[u];                                                            \
+    if (wv != 0.f) {                                                                   \
+      _Pragma("unroll") for (int j = 0; j < R; ++j)                                    \
+      _Pragma("unroll") for (int i = 0; i < PX; ++i) {                                 \
+        acc[j][i] = ffma2(wv, reg[(j - (uu) + 2 * S) % S][i], acc[j][i]);              \
+      }                                                                                \
+    }                                                                                  \
+    _Pragma("unroll") for (int i = 0; i < PX; ++i)                                     \
+      cp_async8(ring_sa + unsigned(((uu) * 32 * PX + 32 * i) * sizeof(float2)),        \
+                pf + 32 * i, (u) + 1 + R < n_steps);                                   \
+    cp_async_commit();                                                                 \
+    pf -= row_step;                                                                    \
+  }
+    const int full = n_steps - n_steps % S;
+    for (int ub = 0; ub < full; ub += S) {
+#pragma unroll
+      for (int uu = 0; uu < S; ++uu) WCGH_LUT_CP_STEP(uu, ub + uu)
+    }
+#pragma unroll
+    for (int uu = 0; uu < S - 1; ++uu) {
+      if (full + uu < n_steps) WCGH_LUT_CP_STEP(uu, full + uu)
+    }
+#undef WCGH_LUT_CP_STEP
+  }
+  cp_async_wait<0>();
 
 #pragma unroll
   for (int j = 0; j < R; ++j) {
@@ -276,18 +444,18 @@ constexpr int kMaxChunkSteps = 4096;
 constexpr size_t kPartialBytes = 2ull << 30;
 
 // Register-window shape: R rows x PX columns per thread, D rows of prefetch,
-// W warps per CTA. Default 8 x 4 x 2 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
+// W warps per CTA. Default 8 x 2 x 4 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
 // another compiled shape (tuning only; results equal up to fp32 rounding).
 struct LutVariant {
-  int R, PX, D, W;
+  int R, PX, D, W, CP;  // CP=1: K4b (cp.async shared ring; D unused)
 };
 LutVariant lut_variant() {
   static const LutVariant v = [] {
-    LutVariant d{8, 4, 2, 4};
+    LutVariant d{8, 2, 4, 4, 0};
     if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
-      int r = 0, px = 0, dd = 0, w = 4;
-      const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
-      if (got >= 3) d = LutVariant{r, px, dd, w};
+      int r = 0, px = 0, dd = 0, w = 4, cp = 0;
+      const int got = std::sscanf(e, "%d,%d,%d,%d,%d", &r, &px, &dd, &w, &cp);
+      if (got >= 3) d = LutVariant{r, px, dd, w, cp};
     }
     return d;
   }();
@@ -311,6 +479,23 @@ void launch_stage_v(const float2* lut, int nh, const StageCells& sc, int off, in
       chunk0, chunk_steps, out, stride);
 }
 
+template <int B, int R, int PX, int W>
+void launch_stage_cp(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
+                     int tiles_x, dim3 grid, int chunk0, int chunk_steps, float2* out,
+                     size_t stride, cudaStream_t s) {
+  const size_t ring = sizeof(float2) * size_t(W) * (R + 1) * 32 * PX;
+  const size_t smem = ring + sizeof(float) * size_t(chunk_steps + sc.m + 32);
+  static bool attr = false;
+  if (!attr) {
+    WCGH_CUDA(cudaFuncSetAttribute(k_lut_stage_cp<B, R, PX, W>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
+  k_lut_stage_cp<B, R, PX, W><<<grid, W * 32, smem, s>>>(
+      lut, nh, sc.runs.as<int4>(), sc.n_runs, sc.dense.as<float>(), off, row0, rows, tiles_x,
+      chunk0, chunk_steps, out, stride);
+}
+
 template <int B>
 void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageCells& sc, int off,
                     int row0, int rows, int tiles_x, dim3 grid, int chunk0, int chunk_steps,
@@ -321,9 +506,26 @@ void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageC
                                        chunk_steps, out, stride, s);                        \
     return;                                                                                 \
   }
+  if (v.CP) {
+    if (v.R == 8 && v.PX == 4 && v.W == 4) {
+      launch_stage_cp<B, 8, 4, 4>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,
+                                  chunk_steps, out, stride, s);
+      return;
+    }
+    if (v.R == 8 && v.PX == 2 && v.W == 4) {
+      launch_stage_cp<B, 8, 2, 4>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,
+                                  chunk_steps, out, stride, s);
+      return;
+    }
+    throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
+  }
   WCGH_V(8, 4, 2, 4)
-  WCGH_V(8, 4, 3, 4)
+  WCGH_V(8, 2, 2, 4)
   WCGH_V(8, 2, 4, 4)
+  WCGH_V(8, 2, 6, 4)
+  WCGH_V(8, 2, 4, 8)
+  WCGH_V(16, 2, 4, 4)
+  WCGH_V(16, 2, 2, 4)
 #undef WCGH_V
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
 }

@@ -1,0 +1,8 @@
+# LUT variant sweep: register ring (R,PX,D,W) vs cp.async shared ring (R,PX,0,W,1)
+mkdir -p gpurun_out
+for v in ${VARIANTS:-"8,4,2,4" "8,4,1,4" "8,2,4,4" "8,4,0,4,1" "8,2,0,4,1"}; do
+  for cfg in 2 1; do
+    r=$(WCGH_LUT_VARIANT=$v timeout 300 python bench.py --config $cfg --method lut --steps 3 --warmup 2 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.2f ms  frac %.3f' % (d['ms_per_step'], d['roofline']['frac']))" 2>&1)
+    echo "variant=$v cfg$cfg lut: $r"
+  done
+done
