@@ -15,11 +15,14 @@
 // and LUT samples are reused from registers:
 //   * cells are listed column-major (per cell column c_x, ascending c_y);
 //   * a thread owns R pixel rows at stride B and PX pixel columns at stride
-//     32 (a CTA of 8 warps covers 8R rows x 32PX columns);
+//     32 (default R = 8, PX = 2); the W = 4 warps of a CTA share one row
+//     residue mod B and take consecutive row groups, so a LUT row one warp
+//     loads is the row the next warp needs R steps later (L1 reuse);
 //   * for cell (c_x, c_y) pixel row j reads LUT row y_j - a_y, and
 //     (y_j + B) - (a_y + B) is the same row: stepping c_y -> c_y + 1 shifts
 //     the R-row register window by one, so each step loads one new LUT row
-//     segment (PX samples) and performs R*PX complex-by-real MACs (2 FFMA each);
+//     segment (PX samples, prefetched D steps ahead) and performs R*PX
+//     complex-by-real MACs, one packed FFMA2 (fma.rn.f32x2) each;
 //   * runs of cells closer than R rows are stepped through; longer gaps
 //     restart the window.
 // Cells are split into fixed chunks of the column-major list; each
@@ -274,283 +277,6 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
   }
 }
 
-// ---- K4b: same tile walk, LUT rows staged once per CTA through a
-// shared-memory row ring (cp.async + mbarrier producer/consumer).
-//
-// The W consumer warps of a CTA cover one row residue at consecutive row
-// groups, so for a run of n steps the CTA needs the LUT rows rho0 + B k for
-// k = WR-1 down to -(n-1): one "stream" of WR + n - 1 row segments
-// (32 PX float2 each), consumed in the same order by every consumer warp:
-//   warp w: skip (W-1-w)R rows, read R rows (its initial register window),
-//           read one row per step for steps 0..n-2 (the row for the next
-//           step), skip wR rows.
-// The streams of the CTA's runs are concatenated and cut into stages of G
-// rows; stream row q lives in ring slot q mod (G NS). A dedicated producer
-// warp (warp W) walks the stream: per stage it waits empty[g mod NS], each
-// lane issues its G x PX 8-byte cp.async and one
-// cp.async.mbarrier.arrive.noinc on full[g mod NS]. Consumers synchronise
-// only at service points (once per R+1 steps and at run boundaries): in
-// stage order they wait full for every stage they will touch before the
-// next service point and arrive on empty for every stage they have
-// finished. Global-load latency is hidden by up to NS stages of lookahead
-// instead of register prefetch, and each LUT row is fetched once per CTA
-// instead of once per warp.
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async8(unsigned dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cp_async(unsigned bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
-               "r"(bytes)
-               : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
-__device__ __forceinline__ void bulk_copy_g2s(unsigned dst, const void* src, unsigned bytes,
-                                              unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred done;\n"
-      "WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
-      " @!done bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-// Q >= (W-1)R + P: a row stays live from warp 0's read to warp W-1's read
-// (W-1)R steps later, plus the production lookahead.
-constexpr int kStageRows = 8;   // G
-constexpr int kRingStages = 8;  // NS (ring of G NS = 64 rows)
-
-// a row slot holds the 16-byte-aligned superset of one 32 PX float2 segment
-template <int PX>
-constexpr int lut_slot_bytes() { return 32 * PX * 8 + 16; }
-template <int R, int PX, int W>
-constexpr size_t lut_sm_static_bytes() {
-  return size_t(kStageRows * kRingStages) * lut_slot_bytes<PX>() +
-         2 * sizeof(unsigned long long) * kRingStages;
-}
-
-template <int B, int R, int PX, int W>
-__global__ void __launch_bounds__((W + 1) * 32, PX == 4 ? 2 : 3)
-    k_lut_stage_sm(const float2* __restrict__ lut, int nh, const int4* __restrict__ runs,
-                   int n_runs, const float* __restrict__ dense, int off, int row0, int rows,
-                   int tiles_x, int chunk0, int chunk_steps, float2* __restrict__ out,
-                   size_t out_stride) {
-  constexpr int S = R + 1;  // register ring: R live diagonals + the next one
-  constexpr int G = kStageRows, NS = kRingStages, QR = G * NS;
-  constexpr int SLOT = lut_slot_bytes<PX>();
-  // a consumer touches at most S rows past its position before it services
-  // again, and warp 0 leads warp W-1 by (W-1)R rows
-  static_assert((W - 1) * R + 2 * S + G <= QR, "row ring too small");
-  static_assert(G <= 32, "one producer lane per stage row");
-  extern __shared__ float4 s_dyn[];
-  char* s_ring = reinterpret_cast<char*>(s_dyn);                          // QR x SLOT bytes
-  unsigned long long* s_full = reinterpret_cast<unsigned long long*>(s_ring + QR * SLOT);
-  unsigned long long* s_empty = s_full + NS;
-  float* s_w = reinterpret_cast<float*>(s_empty + NS);
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx = blockIdx.x % tiles_x, tyc = blockIdx.x / tiles_x;
-  const int r = tyc % B;
-  const int yb0 = (tyc / B) * W * (B * R) + r;  // band row of warp 0's pixel row 0
-  const int span = 2 * nh - 1;
-  const int d_lo = (chunk0 + blockIdx.y) * chunk_steps;
-  const int d_hi = d_lo + chunk_steps;
-
-  auto lower_bound = [&](int key) {
-    int lo = 0, hi = n_runs;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(&runs[mid].w) < key) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-  };
-  const int r_lo = lower_bound(d_lo), r_hi = lower_bound(d_hi);
-  int w_lo = 0;
-  if (r_lo < r_hi) {
-    w_lo = __ldg(&runs[r_lo].w);
-    const int4 lr = __ldg(runs + r_hi - 1);
-    const int w_n = lr.w + lr.z - w_lo;
-    for (int i = threadIdx.x; i < w_n; i += (W + 1) * 32) s_w[i] = __ldg(dense + w_lo + i);
-  }
-  const unsigned full_sa = smem_addr(s_full), empty_sa = smem_addr(s_empty);
-  if (threadIdx.x < NS) {
-    mbar_init(full_sa + 8 * threadIdx.x, 1);
-    mbar_init(empty_sa + 8 * threadIdx.x, W * 32);
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  __syncthreads();
-
-  const long long row_step = (long long)B * span;  // one diagonal (k) in LUT elements
-  if (warp == W) {
-    // ---- producer warp: lane k < G streams row k of each stage with one
-    // bulk copy of the 16-byte-aligned superset of the row segment
-    const int rho_top = row0 + yb0 - off + nh - 1 + B * (W * R - 1);
-    const int xt = tx * (32 * PX);
-    auto run_top = [&](int ri_, int& len_) {
-      const int4 rec = __ldg(runs + ri_);
-      len_ = W * R + rec.z - 1;  // >= WR >= G: at most one run boundary per stage
-      return lut + (xt - off - B * rec.x + nh - 1) + (long long)(rho_top - B * rec.y) * span;
-    };
-    int ri = r_lo, i = 0, len = 0, len_next = 0;
-    const float2* top = lut;
-    const float2* top_next = lut;
-    if (ri < r_hi) top = run_top(ri, len);
-    if (ri + 1 < r_hi) top_next = run_top(ri + 1, len_next);
-    const unsigned ring_sa = smem_addr(s_ring);
-    for (int g = 0; ri < r_hi; ++g) {
-      const int slot = g % NS;
-      if (g >= NS) mbar_wait(empty_sa + 8 * slot, ((g / NS) - 1) & 1);
-      const int ik = i + lane;
-      const float2* src = nullptr;
-      if (lane < G) {
-        if (ik < len) src = top - (long long)ik * row_step;
-        else if (ri + 1 < r_hi) src = top_next - (long long)(ik - len) * row_step;
-      }
-      const unsigned n_valid = __popc(__ballot_sync(0xffffffffu, src != nullptr));
-      const int row_slot = slot * G + lane;
-      const char* a = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-      if (lane == 0) mbar_arrive_expect_tx(full_sa + 8 * slot, n_valid * SLOT);
-      __syncwarp();
-      if (src) bulk_copy_g2s(ring_sa + unsigned(row_slot * SLOT), a, SLOT, full_sa + 8 * slot);
-      i += G;
-      if (i >= len) {
-        i -= len;
-        ++ri;
-        top = top_next;
-        len = len_next;
-        if (ri + 1 < r_hi) top_next = run_top(ri + 1, len_next);
-      }
-    }
-    return;
-  }
-
-  // ---- consumer warps
-  const int yb = yb0 + warp * (B * R);
-  const int x0 = tx * (32 * PX) + lane;
-  float2 acc[R][PX];
-#pragma unroll
-  for (int j = 0; j < R; ++j)
-#pragma unroll
-    for (int i = 0; i < PX; ++i) acc[j][i] = make_float2(0.f, 0.f);
-
-  int q = 0;        // next stream row
-  int v_stage = 0;  // stages [0, v_stage) observed full
-  int a_stage = 0;  // stages [0, a_stage) released (empty arrivals)
-  // make rows [q, q + ahead) readable; release every finished stage
-  auto service = [&](int ahead) {
-    const int target = q + ahead;
-    while (v_stage * G < target) {
-      mbar_wait(full_sa + 8 * (v_stage % NS), (v_stage / NS) & 1);
-      ++v_stage;
-      while (a_stage < v_stage && (a_stage + 1) * G <= q) {
-        mbar_arrive(empty_sa + 8 * (a_stage % NS));
-        ++a_stage;
-      }
-    }
-    while (a_stage < v_stage && (a_stage + 1) * G <= q) {
-      mbar_arrive(empty_sa + 8 * (a_stage % NS));
-      ++a_stage;
-    }
-  };
-  const char* ring = s_ring + lane * sizeof(float2);
-  const int xt = tx * (32 * PX);
-  const int rho_top = row0 + yb0 - off + nh - 1 + B * (W * R - 1);
-
-  for (int ri = r_lo; ri < r_hi; ++ri) {
-    const int4 run = __ldg(runs + ri);
-    const int n_steps = run.z;
-    const float* ws = s_w + (run.w - w_lo);
-    // Row i of this run's stream starts at LUT element
-    // E_i = (xt - off - B cx + nh - 1) + (rho_top - B cy - B i) span; the
-    // producer copied it from the 16-byte boundary below, so it sits 8 (E_i
-    // & 1) bytes into its slot (span is odd: E_i & 1 = (c_par + B i) & 1).
-    const int c_par = (xt - off - B * run.x + nh - 1 + rho_top - B * run.y) & 1;
-    const int q_run = q;  // stream row 0 of this run
-    auto row_ptr = [&](int qq) {
-      const int sh = (c_par ^ ((qq - q_run) * B)) & 1;
-      return reinterpret_cast<const float2*>(ring + (qq & (QR - 1)) * SLOT + 8 * sh);
-    };
-    float2 reg[S][PX];
-    q += (W - 1 - warp) * R;  // rows above this warp's window
-    service(R);
-#pragma unroll
-    for (int t = R - 1; t >= 0; --t) {
-      const float2* src = row_ptr(q + (R - 1 - t));
-#pragma unroll
-      for (int c = 0; c < PX; ++c) reg[t][c] = src[32 * c];
-    }
-    q += R;
-    float w_next = ws[0];
-    // step u: load stream row q0 + u (diagonal -(u+1), used from step u+1
-    // on; past the run's last read it is dead), then MAC with w_u
-#define WCGH_LUT_SM_STEP(uu, u)                                                    \
-  {                                                                                \
-    {                                                                              \
-      const float2* src = row_ptr(q + (uu));                                       \
-      _Pragma("unroll") for (int c = 0; c < PX; ++c)                               \
-        reg[(R - (uu)) % S][c] = src[32 * c];                                      \
-    }                                                                              \
-    const float wv = w_next;                                                       \
-    w_next = ws[(u) + 1];                                                          \
-    if (wv != 0.f) {                                                               \
-      _Pragma("unroll") for (int j = 0; j < R; ++j)                                \
-      _Pragma("unroll") for (int i = 0; i < PX; ++i)                               \
-        acc[j][i] = ffma2(wv, reg[(j - (uu) + 2 * S) % S][i], acc[j][i]);          \
-    }                                                                              \
-  }
-    const int full = n_steps - n_steps % S;
-    for (int ub = 0; ub < full; ub += S) {
-      const int reads = min(S, n_steps - 1 - ub);
-      service(reads);
-#pragma unroll
-      for (int uu = 0; uu < S; ++uu) WCGH_LUT_SM_STEP(uu, ub + uu)
-      q += reads;
-    }
-    if (full < n_steps) {
-      const int reads = n_steps - 1 - full;
-      service(reads);
-#pragma unroll
-      for (int uu = 0; uu < S - 1; ++uu) {
-        if (full + uu < n_steps) WCGH_LUT_SM_STEP(uu, full + uu)
-      }
-      q += reads;
-    }
-#undef WCGH_LUT_SM_STEP
-    q += warp * R;  // rows below this warp's window
-  }
-  service(0);
-
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    const int row = yb + j * B;
-    if (row < rows) {
-      float2* dst = out + size_t(blockIdx.y) * out_stride + size_t(row) * nh;
-#pragma unroll
-      for (int i = 0; i < PX; ++i) {
-        const int x = x0 + 32 * i;
-        if (x < nh) dst[x] = acc[j][i];
-      }
-    }
-  }
-}
-
 // out (+)= sum of `n` partial planes in order, fp64 accumulation.
 __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, size_t count,
                                   int accumulate, float2* __restrict__ out) {
@@ -576,15 +302,15 @@ constexpr size_t kPartialBytes = 2ull << 30;
 // W warps per CTA. Default 8 x 2 x 4 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
 // another compiled shape (tuning only; results equal up to fp32 rounding).
 struct LutVariant {
-  int R, PX, D, W, CP;  // CP=1: K4b (CTA-shared cp.async row ring; D unused)
+  int R, PX, D, W;
 };
 LutVariant lut_variant() {
   static const LutVariant v = [] {
-    LutVariant d{8, 2, 4, 4, 0};
+    LutVariant d{8, 2, 4, 4};
     if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
-      int r = 0, px = 0, dd = 0, w = 4, cp = 0;
-      const int got = std::sscanf(e, "%d,%d,%d,%d,%d", &r, &px, &dd, &w, &cp);
-      if (got >= 3) d = LutVariant{r, px, dd, w, cp};
+      int r = 0, px = 0, dd = 0, w = 4;
+      const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
+      if (got >= 3) d = LutVariant{r, px, dd, w};
     }
     return d;
   }();
@@ -608,22 +334,6 @@ void launch_stage_v(const float2* lut, int nh, const StageCells& sc, int off, in
       chunk0, chunk_steps, out, stride);
 }
 
-template <int B, int R, int PX, int W>
-void launch_stage_sm(const float2* lut, int nh, const StageCells& sc, int off, int row0, int rows,
-                     int tiles_x, dim3 grid, int chunk0, int chunk_steps, float2* out,
-                     size_t stride, cudaStream_t s) {
-  const size_t smem = lut_sm_static_bytes<R, PX, W>() + sizeof(float) * size_t(chunk_steps + sc.m + 32);
-  static bool attr = false;
-  if (!attr) {
-    WCGH_CUDA(cudaFuncSetAttribute(k_lut_stage_sm<B, R, PX, W>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr = true;
-  }
-  k_lut_stage_sm<B, R, PX, W><<<grid, (W + 1) * 32, smem, s>>>(
-      lut, nh, sc.runs.as<int4>(), sc.n_runs, sc.dense.as<float>(), off, row0, rows, tiles_x,
-      chunk0, chunk_steps, out, stride);
-}
-
 template <int B>
 void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageCells& sc, int off,
                     int row0, int rows, int tiles_x, dim3 grid, int chunk0, int chunk_steps,
@@ -633,19 +343,6 @@ void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageC
     launch_stage_v<B, R_, PX_, D_, W_>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0, \
                                        chunk_steps, out, stride, s);                        \
     return;                                                                                 \
-  }
-  if (v.CP) {
-    if (v.R == 8 && v.PX == 4 && v.W == 4) {
-      launch_stage_sm<B, 8, 4, 4>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,
-                                  chunk_steps, out, stride, s);
-      return;
-    }
-    if (v.R == 8 && v.PX == 2 && v.W == 4) {
-      launch_stage_sm<B, 8, 2, 4>(lut, nh, sc, off, row0, rows, tiles_x, grid, chunk0,
-                                  chunk_steps, out, stride, s);
-      return;
-    }
-    throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
   }
   WCGH_V(8, 4, 2, 4)
   WCGH_V(8, 2, 2, 4)
