@@ -235,6 +235,31 @@ int wcgh_read_cgh1(const char* path, float* plane, int64_t capacity, int* n_out,
  * job (row0 = 0, rows = plane_size) as CGH1, scene = layer 0. */
 int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage);
 
+/* ---- Reconstruction and metrics -------------------
+ * fp64 on the device like the reference; n must be a power of two. Complex
+ * arrays are interleaved (re, im); `dtype` selects complex64 input
+ * (WCGH_F32, e.g. a synthesised hologram) or complex128 (WCGH_F64). The
+ * scene's z is ignored where an explicit z_signed is taken. */
+/* fft_2d (fft.cpp:45-68): forward or inverse (scaled by 1/n^2) 2-D DFT. */
+int wcgh_fft_2d(wcgh_ctx* ctx, const double* field, int n, int inverse, double* out);
+/* build_kernel (angular_spectrum.cpp:11-33): transfer function, DC first,
+ * evanescent samples zero; z_signed != 0. */
+int wcgh_propagation_kernel(wcgh_ctx* ctx, const wcgh_layer* scene, int n, double z_signed,
+                            double* out);
+/* propagate (angular_spectrum.cpp:35-45): IDFT(DFT(field) * transfer). */
+int wcgh_propagate(wcgh_ctx* ctx, const void* field, int dtype, int n, const wcgh_layer* scene,
+                   double z_signed, double* out);
+/* reconstruct (angular_spectrum.cpp:47-61): back-propagate by -scene.z and
+ * return |.| (intensity = 0) or |.|^2, n x n doubles. */
+int wcgh_reconstruct(wcgh_ctx* ctx, const void* hologram, int dtype, int n,
+                     const wcgh_layer* scene, int intensity, double* out);
+/* Same on the last run's plane of a whole-plane job, without a host copy. */
+int wcgh_job_reconstruct(wcgh_job* job, const wcgh_layer* scene, int intensity, double* out);
+/* ssim (metrics.cpp:49-85): mean box-window SSIM of two width x height
+ * images; window in [1, min(width, height)], dynamic_range > 0. */
+int wcgh_ssim(wcgh_ctx* ctx, const double* a, const double* b, int width, int height, int window,
+              double k1, double k2, double dynamic_range, double* score);
+
 /* One-shot: job create + upload + run + download + destroy. The entry the
  * C++ synthesize_progressive mirror calls (synthesis.hpp:88-91). */
 int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object,

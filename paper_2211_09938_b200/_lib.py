@@ -90,6 +90,13 @@ _SIGS = [
     ("wcgh_write_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int, C.POINTER(Layer)]),
     ("wcgh_read_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int64, C.POINTER(C.c_int), C.POINTER(Layer)]),
     ("wcgh_job_write_cgh1", C.c_int, [_VP, C.c_char_p, C.c_int]),
+    ("wcgh_fft_2d", C.c_int, [_VP, _VP, C.c_int, C.c_int, _VP]),
+    ("wcgh_propagation_kernel", C.c_int, [_VP, C.POINTER(Layer), C.c_int, C.c_double, _VP]),
+    ("wcgh_propagate", C.c_int, [_VP, _VP, C.c_int, C.c_int, C.POINTER(Layer), C.c_double, _VP]),
+    ("wcgh_reconstruct", C.c_int, [_VP, _VP, C.c_int, C.c_int, C.POINTER(Layer), C.c_int, _VP]),
+    ("wcgh_job_reconstruct", C.c_int, [_VP, C.POINTER(Layer), C.c_int, _VP]),
+    ("wcgh_ssim", C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                            C.c_double, C.POINTER(C.c_double)]),
     ("wcgh_synthesize", C.c_int, [_VP, C.POINTER(Desc), _VP, _VP, _VP, C.POINTER(Stats)]),
 ]
 EXPORTED = [s[0] for s in _SIGS]

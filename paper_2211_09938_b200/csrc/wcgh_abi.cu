@@ -56,6 +56,8 @@ struct wcgh_ctx {
   DevBuf b_in, b_in2, b_out, b_out2, b_misc, b_pts, b_plane, b_lut, b_lut_scratch, lut_partial;
   DirectScratch direct;
   StageCells cells;
+  ReconPlan recon;  // reconstruction / FFT entry points
+  DevBuf b_ssim;
   std::mutex mu;
 };
 
@@ -922,6 +924,152 @@ int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage) {
     const int rc = wcgh_write_cgh1(path, host.data(), d.plane_size, &job->layers[0]);
     if (rc == WCGH_EVALIDATION) throw ValidationError(t_last_error);
     if (rc) throw RuntimeError(t_last_error);
+  });
+}
+
+// ---- reconstruction and metrics (angular_spectrum.cpp, fft.cpp, metrics.cpp)
+
+namespace {
+void require_fft_side(int n) {
+  require(n >= 1 && is_pow2(n), "fft_2d: side must be a power of two");
+}
+void require_complex_dtype(int dtype) {
+  require(dtype == WCGH_F32 || dtype == WCGH_F64,
+          "field: dtype must be WCGH_F32 (complex64) or WCGH_F64 (complex128)");
+}
+void require_optics(const wcgh_layer* scene) {
+  require(scene != nullptr, "scene: NULL");
+  require(scene->wavelength > 0.0, "scene: wavelength must be positive");
+  require(scene->pitch > 0.0, "scene: pitch must be positive");
+}
+}  // namespace
+
+int wcgh_fft_2d(wcgh_ctx* ctx, const double* field, int n, int inverse, double* out) {
+  return guard(ctx, [&] {
+    require(ctx && field && out, "fft_2d: NULL argument");
+    require_fft_side(n);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t bytes = sizeof(double2) * size_t(n) * n;
+    double2* f = recon_field(ctx->recon, n);
+    WCGH_CUDA(cudaMemcpyAsync(f, field, bytes, cudaMemcpyHostToDevice, s));
+    launch_fft2d(ctx->recon, n, inverse != 0, s);
+    WCGH_CUDA(cudaMemcpyAsync(out, f, bytes, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_propagation_kernel(wcgh_ctx* ctx, const wcgh_layer* scene, int n, double z_signed,
+                            double* out) {
+  return guard(ctx, [&] {
+    require(ctx && out, "build_kernel: NULL argument");
+    require_optics(scene);
+    require(z_signed != 0.0, "build_kernel: |z| must be positive");
+    require_fft_side(n);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    double2* f = recon_field(ctx->recon, n);
+    launch_transfer(n, scene->wavelength, scene->pitch, z_signed, f, s);
+    WCGH_CUDA(cudaMemcpyAsync(out, f, sizeof(double2) * size_t(n) * n, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_propagate(wcgh_ctx* ctx, const void* field, int dtype, int n, const wcgh_layer* scene,
+                   double z_signed, double* out) {
+  return guard(ctx, [&] {
+    require(ctx && field && out, "propagate: NULL argument");
+    require_optics(scene);
+    require(z_signed != 0.0, "build_kernel: |z| must be positive");
+    require_complex_dtype(dtype);
+    require_fft_side(n);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t nn = size_t(n) * n;
+    const bool single = dtype == WCGH_F32;
+    void* in = ctx->b_in.reserve((single ? sizeof(float2) : sizeof(double2)) * nn);
+    WCGH_CUDA(cudaMemcpyAsync(in, field, (single ? sizeof(float2) : sizeof(double2)) * nn,
+                              cudaMemcpyHostToDevice, s));
+    load_field(ctx->recon, in, single, n, s);
+    launch_propagate(ctx->recon, n, scene->wavelength, scene->pitch, z_signed, true, s);
+    WCGH_CUDA(cudaMemcpyAsync(out, ctx->recon.field.p, sizeof(double2) * nn, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_reconstruct(wcgh_ctx* ctx, const void* hologram, int dtype, int n,
+                     const wcgh_layer* scene, int intensity, double* out) {
+  return guard(ctx, [&] {
+    require(ctx && hologram && out, "reconstruct: NULL argument");
+    require_optics(scene);
+    require(scene->z != 0.0, "build_kernel: |z| must be positive");
+    require_complex_dtype(dtype);
+    require_fft_side(n);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t nn = size_t(n) * n;
+    const bool single = dtype == WCGH_F32;
+    void* in = ctx->b_in.reserve((single ? sizeof(float2) : sizeof(double2)) * nn);
+    WCGH_CUDA(cudaMemcpyAsync(in, hologram, (single ? sizeof(float2) : sizeof(double2)) * nn,
+                              cudaMemcpyHostToDevice, s));
+    load_field(ctx->recon, in, single, n, s);
+    double* img = static_cast<double*>(ctx->b_out.reserve(sizeof(double) * nn));
+    launch_reconstruct(ctx->recon, n, scene->wavelength, scene->pitch, scene->z, intensity != 0,
+                       img, s);
+    WCGH_CUDA(cudaMemcpyAsync(out, img, sizeof(double) * nn, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_job_reconstruct(wcgh_job* job, const wcgh_layer* scene, int intensity, double* out) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && out, "reconstruct: NULL argument");
+    require_optics(scene);
+    require(scene->z != 0.0, "build_kernel: |z| must be positive");
+    const int n = job->desc.plane_size;
+    require(job->desc.row0 == 0 && job->desc.rows == n,
+            "reconstruct: the job must hold the whole plane (row0 = 0, rows = plane_size)");
+    wcgh_ctx* ctx = job->ctx;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t nn = size_t(n) * n;
+    load_field(ctx->recon, job->plane.p, true, n, s);
+    double* img = static_cast<double*>(ctx->b_out.reserve(sizeof(double) * nn));
+    launch_reconstruct(ctx->recon, n, scene->wavelength, scene->pitch, scene->z, intensity != 0,
+                       img, s);
+    WCGH_CUDA(cudaMemcpyAsync(out, img, sizeof(double) * nn, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_ssim(wcgh_ctx* ctx, const double* a, const double* b, int width, int height, int window,
+              double k1, double k2, double dynamic_range, double* score) {
+  return guard(ctx, [&] {
+    require(ctx && a && b && score, "ssim: NULL argument");
+    require(width >= 1 && height >= 1, "ssim: image sizes differ");
+    require(window > 0 && window <= std::min(width, height),
+            "ssim: window must fit inside the images");
+    require(dynamic_range > 0.0, "ssim: dynamic range must be positive");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    use_device(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t nn = size_t(width) * height;
+    double* da = static_cast<double*>(ctx->b_in.reserve(sizeof(double) * nn));
+    double* db = static_cast<double*>(ctx->b_in2.reserve(sizeof(double) * nn));
+    double* dr = static_cast<double*>(ctx->b_misc.reserve(sizeof(double)));
+    WCGH_CUDA(cudaMemcpyAsync(da, a, sizeof(double) * nn, cudaMemcpyHostToDevice, s));
+    WCGH_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * nn, cudaMemcpyHostToDevice, s));
+    launch_ssim(da, db, width, height, window, k1, k2, dynamic_range, ctx->b_ssim, dr, s);
+    double total = 0.0;
+    WCGH_CUDA(cudaMemcpyAsync(&total, dr, sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    const double count = double(width - window + 1) * double(height - window + 1);
+    *score = total / count;
   });
 }
 

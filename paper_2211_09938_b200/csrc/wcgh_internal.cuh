@@ -217,6 +217,31 @@ void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cu
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
                          int rows, float2* out, cudaStream_t stream, DirectTiming* timing);
 
+// ---- reconstruction and SSIM (K6, K7) --------------
+struct ReconPlan {
+  int n = 0;
+  int plan = 0;  // cufftHandle (Z2Z, n x n)
+  DevBuf field;  // n x n double2 working field
+  ReconPlan() = default;
+  ReconPlan(const ReconPlan&) = delete;
+  ReconPlan& operator=(const ReconPlan&) = delete;
+  ~ReconPlan();
+};
+double2* recon_field(ReconPlan& rp, int n);
+// field <- device input (complex64 if single, else complex128)
+void load_field(ReconPlan& rp, const void* dev_in, bool single, int n, cudaStream_t s);
+int launch_fft2d(ReconPlan& rp, int n, bool inverse, cudaStream_t s);
+int launch_transfer(int n, double wavelength, double pitch, double z_signed, double2* out,
+                    cudaStream_t s);
+// field <- IDFT(DFT(field) * transfer), scaled by 1/n^2 when `scaled`
+int launch_propagate(ReconPlan& rp, int n, double wavelength, double pitch, double z_signed,
+                     bool scaled, cudaStream_t s);
+int launch_reconstruct(ReconPlan& rp, int n, double wavelength, double pitch, double z,
+                       bool intensity, double* out, cudaStream_t s);
+// *result = sum of window scores (divide by the window count on the host)
+int launch_ssim(const double* a, const double* b, int w, int h, int window, double k1, double k2,
+                double dynamic_range, DevBuf& scratch, double* result, cudaStream_t s);
+
 // LUT supports live in guarded allocations: zeroed guard rows before
 // (prefetch below row 0: <= B*(D+1)+1 rows) and after (a CTA's last row
 // groups overhang the band by < B*R*W rows; they compute on guard data and are

@@ -110,6 +110,16 @@ class HologramJob:
         L.check(self.ctx.lib.wcgh_job_download_stages(self.h, L.ptr(out)))
         return out
 
+    def reconstruct(self, layer=None, intensity: bool = False) -> np.ndarray:
+        """reconstruct (angular_spectrum.cpp:47-61) of the last run's plane on the
+        device (whole-plane jobs); layer = (wavelength, pitch, z), default layer 0."""
+        n = self.spec.plane_size
+        lay = L.Layer(*(layer if layer is not None else self.spec.layers[0]))
+        out = np.empty((n, n))
+        L.check(self.ctx.lib.wcgh_job_reconstruct(self.h, C.byref(lay), int(bool(intensity)),
+                                                  L.ptr(out)))
+        return out
+
     def plane_dev_ptr(self) -> int:
         return int(self.ctx.lib.wcgh_job_plane_dev(self.h) or 0)
 

@@ -173,3 +173,77 @@ def read_cgh1(path):
     plane = np.empty((n.value, n.value), np.complex64)
     L.check(lib.wcgh_read_cgh1(str(path).encode(), L.ptr(plane), plane.size, C.byref(n), C.byref(lay)))
     return plane, (lay.wavelength, lay.pitch, lay.z)
+
+
+# ---- reconstruction and metrics (angular_spectrum.cpp, fft.cpp, metrics.cpp) ----
+
+def _complex_in(field: np.ndarray):
+    field = np.ascontiguousarray(field)
+    if field.dtype == np.complex64:
+        return field, L.F32
+    if field.dtype == np.complex128:
+        return field, L.F64
+    return np.ascontiguousarray(field, np.complex128), L.F64
+
+
+def _square_side(field: np.ndarray, what: str) -> int:
+    if field.ndim != 2 or field.shape[0] != field.shape[1]:
+        raise L.ValidationError(f"{what}: field must be square")
+    return field.shape[0]
+
+
+def fft_2d(field: np.ndarray, inverse: bool = False, ctx=None) -> np.ndarray:
+    """fft_2d (fft.cpp:45-68) on the device: complex128 in and out."""
+    f = np.ascontiguousarray(field, np.complex128)
+    n = _square_side(f, "fft_2d")
+    out = np.empty_like(f)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_fft_2d(c.h, L.ptr(f), n, int(bool(inverse)), L.ptr(out)))
+    return out
+
+
+def propagation_kernel(layer, n: int, z_signed: float, ctx=None) -> np.ndarray:
+    """build_kernel (angular_spectrum.cpp:11-33) transfer samples, DC first."""
+    out = np.empty((n, n), np.complex128)
+    lay = L.Layer(*layer)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_propagation_kernel(c.h, C.byref(lay), n, float(z_signed), L.ptr(out)))
+    return out
+
+
+def propagate(field: np.ndarray, layer, z_signed: float, ctx=None) -> np.ndarray:
+    """propagate (angular_spectrum.cpp:35-45): complex64 or complex128 field."""
+    f, dt = _complex_in(field)
+    n = _square_side(f, "propagate")
+    out = np.empty((n, n), np.complex128)
+    lay = L.Layer(*layer)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_propagate(c.h, L.ptr(f), dt, n, C.byref(lay), float(z_signed), L.ptr(out)))
+    return out
+
+
+def reconstruct(hologram: np.ndarray, layer, intensity: bool = False, ctx=None) -> np.ndarray:
+    """reconstruct (angular_spectrum.cpp:47-61): back-propagate by -z, |.| or |.|^2."""
+    f, dt = _complex_in(hologram)
+    n = _square_side(f, "reconstruct")
+    out = np.empty((n, n))
+    lay = L.Layer(*layer)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_reconstruct(c.h, L.ptr(f), dt, n, C.byref(lay), int(bool(intensity)),
+                                   L.ptr(out)))
+    return out
+
+
+def ssim(a: np.ndarray, b: np.ndarray, window: int = 8, k1: float = 0.01, k2: float = 0.03,
+         dynamic_range: float = 1.0, ctx=None) -> float:
+    """ssim (metrics.cpp:49-85): mean box-window SSIM on the device."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    if a.shape != b.shape or a.ndim != 2:
+        raise L.ValidationError("ssim: image sizes differ")
+    h, w = a.shape
+    out = C.c_double(0.0)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_ssim(c.h, L.ptr(a), L.ptr(b), w, h, int(window), float(k1), float(k2),
+                            float(dynamic_range), C.byref(out)))
+    return float(out.value)

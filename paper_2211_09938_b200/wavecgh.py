@@ -11,6 +11,10 @@ free functions and types (paths under /root/reference/proj):
   synthesis.hpp:18-104   RefinementPlan, GateMask, ProgressiveResult, GridCell,
                          apply_block, synthesize_base, refine,
                          synthesize_progressive, synthesize_pointwise_oracle
+  fft.hpp, angular_spectrum.hpp, metrics.hpp
+                         fft_2d, PropagationKernel, build_kernel, propagate,
+                         reconstruct, ssim, StageMetrics, MetricsReport,
+                         build_report (the validation step after the path)
 
 Images are numpy arrays indexed [y, x] (RealImage/ComplexField are row-major
 with at(x, y)). Every hot-path call runs on the sm_100a kernels through the
@@ -532,3 +536,116 @@ def synthesize_pointwise_oracle(object_: np.ndarray, scene: SceneParams, counter
     ops = stages.apply_blocks(plane, scene.layer(), 1, np.arange(n * n), obj.ravel())
     counter.add(OpLevel.POINTWISE_ORACLE, ops)
     return plane.astype(np.complex128)
+
+
+# ---- fft.hpp / angular_spectrum.hpp / metrics.hpp (validation, on the device) ----
+
+STAGE_NAMES = ["base_LLL", "after_LL", "after_L", "after_full"]  # synthesis.hpp:56-57
+
+
+def _field(field_: np.ndarray, what: str) -> np.ndarray:
+    f = np.asarray(field_)
+    if f.ndim != 2:
+        raise ValidationError(f"{what}: field must be 2-D")
+    return f
+
+
+def fft_2d(field_: np.ndarray, inverse: bool) -> np.ndarray:
+    """fft.cpp:45-68: 2-D DFT (inverse scaled by 1/n^2); square power-of-two side."""
+    f = _field(field_, "fft_2d")
+    if f.shape[0] != f.shape[1]:
+        raise ValidationError("fft_2d: field must be square")
+    if not is_power_of_two(f.shape[0]):
+        raise ValidationError("fft_2d: side must be a power of two")
+    return stages.fft_2d(f, inverse)
+
+
+@dataclass
+class PropagationKernel:
+    """angular_spectrum.hpp:11-15"""
+    scene: SceneParams
+    z_signed: float
+    transfer: np.ndarray
+
+
+def build_kernel(scene: SceneParams, z_signed: float) -> PropagationKernel:
+    """angular_spectrum.cpp:11-33"""
+    if z_signed == 0.0:
+        raise ValidationError("build_kernel: |z| must be positive")
+    t = stages.propagation_kernel(scene.layer(), scene.plane_size(), z_signed)
+    return PropagationKernel(scene, float(z_signed), t)
+
+
+def propagate(field_: np.ndarray, kernel: PropagationKernel) -> np.ndarray:
+    """angular_spectrum.cpp:35-45: IDFT(DFT(field) * transfer). The device
+    evaluates the transfer function of (kernel.scene, kernel.z_signed) on the
+    fly, i.e. kernel.transfer as build_kernel made it."""
+    f = _field(field_, "propagate")
+    if f.shape != kernel.transfer.shape:
+        raise ValidationError("propagate: field size does not match kernel")
+    return stages.propagate(f, kernel.scene.layer(), kernel.z_signed)
+
+
+def reconstruct(hologram: np.ndarray, scene: SceneParams, intensity: bool = False) -> np.ndarray:
+    """angular_spectrum.cpp:47-61"""
+    h = _field(hologram, "reconstruct")
+    n = scene.plane_size()
+    if h.shape != (n, n):
+        raise ValidationError("reconstruct: hologram size does not match scene")
+    return stages.reconstruct(h, scene.layer(), intensity)
+
+
+def ssim(a: np.ndarray, b: np.ndarray, window: int, k1: float, k2: float,
+         dynamic_range: float) -> float:
+    """metrics.cpp:49-85"""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.shape != b.shape:
+        raise ValidationError("ssim: image sizes differ")
+    if window <= 0 or window > min(a.shape):
+        raise ValidationError("ssim: window must fit inside the images")
+    if not dynamic_range > 0.0:
+        raise ValidationError("ssim: dynamic range must be positive")
+    return stages.ssim(a, b, window, k1, k2, dynamic_range)
+
+
+@dataclass
+class StageMetrics:
+    """metrics.hpp:17-22"""
+    name: str = ""
+    ssim: float = 0.0
+    ops: int = 0
+    ops_cumulative: int = 0
+
+
+@dataclass
+class MetricsReport:
+    """metrics.hpp:26-37"""
+    stages: list = field(default_factory=list)
+    pointwise_ops: int = 0
+    window: int = 8
+    k1: float = 0.01
+    k2: float = 0.03
+    dynamic_range: float = 1.0
+    intensity: bool = False
+
+
+def build_report(result: ProgressiveResult, oracle_recon: np.ndarray, scene: SceneParams,
+                 intensity: bool = False) -> MetricsReport:
+    """metrics.cpp:87-112: per-stage SSIM of the reconstructions against the
+    oracle reconstruction, dynamic range = the oracle's value range."""
+    report = MetricsReport(intensity=intensity)
+    report.pointwise_ops = scene.plane_size() * scene.plane_size()
+    lo, hi = float(np.min(oracle_recon)), float(np.max(oracle_recon))
+    report.dynamic_range = hi - lo if hi - lo > 0.0 else 1.0
+    cumulative = 0
+    for s in range(4):
+        recon = reconstruct(result.stage(s), scene, intensity)
+        m = StageMetrics(name=STAGE_NAMES[s])
+        m.ssim = ssim(recon, oracle_recon, report.window, report.k1, report.k2,
+                      report.dynamic_range)
+        m.ops = result.ops.get(STAGE_OP_LEVELS[s])
+        cumulative += m.ops
+        m.ops_cumulative = cumulative
+        report.stages.append(m)
+    return report

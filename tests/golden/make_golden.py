@@ -98,6 +98,40 @@ def main():
     vals = np.array([O.ref_point_fringe(WL, 8e-6, 0.1, 256, dx, dy) for dx, dy in pts])
     save("ref_point_fringe", offsets=np.array(pts, np.int32), values=vals)
 
+    # 8. Reconstruction + SSIM (angular_spectrum.cpp:47-61, metrics.cpp:49-85):
+    #    random complex fields as in test_angular_spectrum.cpp:20-28, the
+    #    config-0 reference hologram, the bright-square hologram of
+    #    test_angular_spectrum.cpp:140-150, and SSIM pairs of test_metrics.cpp.
+    rec = {}
+    for n, seed in ((16, 3), (32, 99)):
+        f = (O.ref_random_image(n, n, seed) - 0.5) + 1j * (O.ref_random_image(n, n, seed + 1) - 0.5)
+        rec[f"field{n}"] = f
+        rec[f"mag{n}"] = O.ref_reconstruct(f, WL, 8e-6, 0.1, False)
+        rec[f"int{n}"] = O.ref_reconstruct(f, WL, 8e-6, 0.1, True)
+    g0 = np.load(OUT / "ref_cfg0.npz")
+    rec["cfg0_recon"] = O.ref_reconstruct(g0["after_full"], WL, 8e-6, 0.2, False)
+    rec["cfg0_base_recon"] = O.ref_reconstruct(g0["base"], WL, 8e-6, 0.2, False)
+    dr = float(rec["cfg0_recon"].max() - rec["cfg0_recon"].min())
+    rec["cfg0_base_ssim"] = np.array(O.ref_ssim(rec["cfg0_base_recon"], rec["cfg0_recon"], 8, 0.01,
+                                                0.03, dr))
+    sq = np.zeros((32, 32))
+    sq[12:20, 12:20] = 1.0
+    rec["square_holo"] = O.ref_pointwise_hologram_reference(sq, WL, 8e-6, 0.01)
+    rec["square_recon"] = O.ref_reconstruct(rec["square_holo"], WL, 8e-6, 0.01, False)
+    pairs = [(16, 5000, 6000, 8), (16, 5001, 6001, 8), (8, 7000, 7001, 8), (24, 3000, 4000, 3),
+             (24, 3001, 4001, 16), (32, 11, 12, 1)]
+    sa, sb, sw, sv = [], [], [], []
+    for n, s1, s2, win in pairs:
+        a = O.ref_random_image(n, n, s1)
+        b = O.ref_random_image(n, n, s2)
+        sa.append(a.ravel()), sb.append(b.ravel()), sw.append((n, win))
+        sv.append(O.ref_ssim(a, b, win, 0.01, 0.03, 1.0))
+    rec["ssim_a"] = np.concatenate(sa)
+    rec["ssim_b"] = np.concatenate(sb)
+    rec["ssim_shape"] = np.array(sw, np.int32)
+    rec["ssim_value"] = np.array(sv)
+    save("ref_recon_ssim", **rec)
+
 
 if __name__ == "__main__":
     main()

@@ -3,14 +3,15 @@ every method's whole hologram against the fp64 FFT oracle (oracle.fft_hologram,
 pinned to the reference and to the direct Eq.(1) oracle in
 test_oracle_pins.py): relative L2 <= 1e-4 over all 16.8 M pixels and SSIM
 >= 0.999 between angular-spectrum reconstructions (angular_spectrum.cpp:46-61,
-metrics.cpp:50-85, dynamic range of the reference reconstruction)."""
+metrics.cpp:50-85, dynamic range of the reference reconstruction), computed
+both by the fp64 CPU oracle and by the device path (csrc/wcgh_recon.cu)."""
 import functools
 
 import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2211_09938_b200 import scenes
+from paper_2211_09938_b200 import scenes, stages
 from paper_2211_09938_b200.hologram import HologramJob, spec_for_scene
 
 pytestmark = pytest.mark.gpu
@@ -37,6 +38,12 @@ def test_full_plane_4096(ctx, cfg, method):
     holo = HologramJob(spec_for_scene(sc, method=method))(sc.objects, sc.masks)
     err = O.rel_l2(holo, ref)
     assert err <= REL_L2, err
+    dr = float(ref_rec.max() - ref_rec.min())
     rec = O.reconstruct(holo, c.wavelength, c.pitch, c.depths[0])
-    s = O.ssim(rec, ref_rec, 8, 0.01, 0.03, float(ref_rec.max() - ref_rec.min()))
+    s = O.ssim(rec, ref_rec, 8, 0.01, 0.03, dr)
     assert s >= 0.999, s
+    # the same check on the device (K6/K7): reconstruction and SSIM agree
+    # with the fp64 CPU path to rounding
+    rec_gpu = stages.reconstruct(holo, (c.wavelength, c.pitch, c.depths[0]))
+    assert np.abs(rec_gpu - rec).max() <= 1e-10 * rec.max()
+    assert abs(stages.ssim(rec_gpu, ref_rec, 8, 0.01, 0.03, dr) - s) <= 1e-9

@@ -152,3 +152,23 @@ def test_fft_oracle_matches_reference_and_direct_sum():
     px, py = rng.integers(0, 256, 300), rng.integers(0, 256, 300)
     ref = O.direct_pixels(xs, ys, amps, lay, [(WL, 8e-6, 0.2)], px, py)
     assert O.max_rel_error(h[py, px], ref) <= 1e-10
+
+
+def test_recon_and_ssim_oracles_match_reference_goldens():
+    """oracle.reconstruct (numpy fp64 FFT) and oracle.ssim (C restatement of
+    metrics.cpp:49-85) against the reference's own outputs."""
+    g = golden("ref_recon_ssim")
+    for n in (16, 32):
+        for key, inten in (("mag", False), ("int", True)):
+            r = O.reconstruct(g[f"field{n}"], WL, 8e-6, 0.1, intensity=inten)
+            ref = g[f"{key}{n}"]
+            assert np.abs(r - ref).max() <= 1e-12 * np.abs(ref).max()
+    g0 = golden("ref_cfg0")
+    r = O.reconstruct(g0["after_full"], WL, 8e-6, 0.2)
+    assert np.abs(r - g["cfg0_recon"]).max() <= 1e-11 * g["cfg0_recon"].max()
+    off = 0
+    for (n, win), v in zip(g["ssim_shape"], g["ssim_value"]):
+        a = g["ssim_a"][off:off + n * n].reshape(n, n)
+        b = g["ssim_b"][off:off + n * n].reshape(n, n)
+        off += n * n
+        assert abs(O.ssim(a, b, int(win)) - v) <= 1e-12
