@@ -8,6 +8,7 @@
 #include <cstring>
 #include <vector>
 
+#include "wavecgh/angular_spectrum.hpp"
 #include "wavecgh/errors.hpp"
 #include "wavecgh/fringe_lut.hpp"
 #include "wavecgh/haar.hpp"
@@ -24,6 +25,8 @@ int ref_synthesize_progressive(const double* object, const double* saliency, int
 int ref_synthesize_pointwise_oracle(const double* object, int n, double wl, double pitch, double z,
                                     int workers, double* out, std::uint64_t* ops);
 int ref_random_image(int w, int h, std::uint64_t seed, double* out);
+int ref_reconstruct(const double* holo, int n, double wl, double pitch, double z, int intensity,
+                    double* out);
 int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx, int cy,
                     double w_re, double w_im, double* plane, std::uint64_t* ops);
 }
@@ -120,6 +123,41 @@ int main() {
     ref_apply_block(wl, pitch, z, n, 2, 1, 2, 0.3, -0.7, pl.data(), &aops);
     EXPECT(rel_l2(plane, pl.data()) <= 1e-5, "apply_block complex weight n=%d", n);
     EXPECT(ac.get(OpLevel::kRefineL) == 1, "apply_block count");
+  }
+  // reconstruct of a synthesised hologram (angular_spectrum.cpp:47-61), fp64 on the device
+  {
+    const int n = 64;
+    const SceneParams scene = make_scene(wl, pitch, z, n);
+    const LutSet luts = LutSet::build(scene);
+    const ProgressiveResult r =
+        synthesize_progressive(random_image(n, 5), random_image(n, 6), scene, RefinementPlan{}, luts);
+    for (bool inten : {false, true}) {
+      const RealImage img = reconstruct(r.after_full, scene, inten);
+      std::vector<double> ref(std::size_t(n) * n);
+      ref_reconstruct(reinterpret_cast<const double*>(r.after_full.data().data()), n, wl, pitch, z,
+                      inten ? 1 : 0, ref.data());
+      double md = 0, mr = 0;
+      for (std::size_t i = 0; i < ref.size(); ++i) {
+        md = std::max(md, std::abs(img.data()[i] - ref[i]));
+        mr = std::max(mr, std::abs(ref[i]));
+      }
+      EXPECT(md <= 1e-11 * mr, "reconstruct intensity=%d max rel %.3e", int(inten), md / mr);
+    }
+    const PropagationKernel k = build_kernel(scene, -z);
+    const ComplexField back = propagate(propagate(r.after_full, build_kernel(scene, z)), k);
+    double md = 0, mr = 0;
+    for (std::size_t i = 0; i < back.size(); ++i) {
+      md = std::max(md, std::abs(back.data()[i] - r.after_full.data()[i]));
+      mr = std::max(mr, std::abs(r.after_full.data()[i]));
+    }
+    EXPECT(md <= 1e-10 * mr, "propagate round trip %.3e", md / mr);
+    bool threw = false;
+    try {
+      build_kernel(scene, 0.0);
+    } catch (const ValidationError&) {
+      threw = true;
+    }
+    EXPECT(threw, "build_kernel(0) must throw ValidationError");
   }
   // validation behaviour (synthesis.cpp:184-202)
   {

@@ -1,9 +1,10 @@
 // Drop-in GPU implementation of the reference's hot-path C++ API.
 //
 // Compile this file INSTEAD OF the reference's core/src/synthesis.cpp,
-// core/src/haar.cpp and core/src/saliency.cpp (keep the reference headers and
-// its other sources) and link libwcgh.so: every entry point keeps its
-// signature (synthesis.hpp:70-104, haar.hpp:36-51, saliency.hpp:25-30) and its
+// core/src/haar.cpp, core/src/saliency.cpp and core/src/angular_spectrum.cpp
+// (keep the reference headers and its other sources) and link libwcgh.so:
+// every entry point keeps its signature (synthesis.hpp:70-104,
+// haar.hpp:36-51, saliency.hpp:25-30, angular_spectrum.hpp:17-27) and its
 // ValidationError behaviour, and runs on the sm_100a kernels through the C ABI
 // (include/wcgh.h). There is no CPU fallback: without a CUDA device the calls
 // throw IoError (the reference's exit-code-2 class).
@@ -13,7 +14,11 @@
 //    reference's complex<double> (relative L2 ~1e-6 vs the fp64 reference);
 //  * `workers` is accepted and ignored (results are launch-invariant);
 //  * random_phase_seed is rejected (complex amplitudes are out of scope,
-//    DESIGN.md §7); random_phase_field itself stays a host RNG function.
+//    DESIGN.md §7); random_phase_field itself stays a host RNG function;
+//  * build_kernel / propagate / reconstruct run in fp64 like the reference
+//    (cuFFT Z2Z); propagate evaluates the transfer function of
+//    (kernel.scene, kernel.z_signed) on the device, i.e. kernel.transfer as
+//    build_kernel made it.
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -24,6 +29,7 @@
 #include <string>
 #include <vector>
 
+#include "wavecgh/angular_spectrum.hpp"
 #include "wavecgh/errors.hpp"
 #include "wavecgh/haar.hpp"
 #include "wavecgh/saliency.hpp"
@@ -375,6 +381,42 @@ ComplexField random_phase_field(const RealImage& amplitude, std::uint64_t seed) 
   ComplexField out(amplitude.width(), amplitude.height());
   for (std::size_t i = 0; i < out.size(); ++i) out.data()[i] = std::polar(amplitude.data()[i], angle(rng));
   return out;
+}
+
+// ---- angular_spectrum.cpp:11-61 ---------------------------------------------
+
+PropagationKernel build_kernel(const SceneParams& scene, double z_signed) {
+  if (z_signed == 0.0) throw ValidationError("build_kernel: |z| must be positive");
+  const int n = scene.plane_size();
+  const wcgh_layer L = layer_of(scene);
+  ComplexField transfer(n, n);
+  check(wcgh_propagation_kernel(gpu(), &L, n, z_signed,
+                                reinterpret_cast<double*>(transfer.data().data())));
+  return PropagationKernel{scene, z_signed, std::move(transfer)};
+}
+
+ComplexField propagate(const ComplexField& field, const PropagationKernel& kernel) {
+  if (!field.same_size(kernel.transfer)) {
+    throw ValidationError("propagate: field size does not match kernel");
+  }
+  const int n = field.width();
+  const wcgh_layer L = layer_of(kernel.scene);
+  ComplexField out(n, n);
+  check(wcgh_propagate(gpu(), field.data().data(), WCGH_F64, n, &L, kernel.z_signed,
+                       reinterpret_cast<double*>(out.data().data())));
+  return out;
+}
+
+RealImage reconstruct(const ComplexField& hologram, const SceneParams& scene, bool intensity) {
+  if (hologram.width() != scene.plane_size() || hologram.height() != scene.plane_size()) {
+    throw ValidationError("reconstruct: hologram size does not match scene");
+  }
+  const int n = hologram.width();
+  const wcgh_layer L = layer_of(scene);
+  std::vector<double> img(std::size_t(n) * n);
+  check(wcgh_reconstruct(gpu(), hologram.data().data(), WCGH_F64, n, &L, intensity ? 1 : 0,
+                         img.data()));
+  return RealImage(n, n, std::move(img));
 }
 
 }  // namespace wavecgh

@@ -1,6 +1,6 @@
 """The reference's own C++ API backed by the GPU (integration/wavecgh_gpu.cpp
-replacing synthesis.cpp, haar.cpp, saliency.cpp) against the unmodified CPU
-reference. The binary is built here by integration/Makefile (it needs the
+replacing synthesis.cpp, haar.cpp, saliency.cpp, angular_spectrum.cpp) against
+the unmodified CPU reference. The binary is built here by integration/Makefile (it needs the
 reference headers) and travels to the GPU box prebuilt."""
 import subprocess
 from pathlib import Path
