@@ -212,6 +212,10 @@ int wcgh_job_upload_dev(wcgh_job* job, const void* object_dev, const void* salie
  * plane. Returns after the work is enqueued AND complete (synchronous). */
 int wcgh_job_run(wcgh_job* job);
 /* D2H of the row band: rows x Nh complex64. */
+/* Front end only (K1/K2: DWT, saliency, gates, A_eff, compaction or run
+ * lists): fills the stats' ops, n_points (compacted points, or nonzero gated
+ * cells for the LUT method) and ms_analysis; no synthesis. */
+int wcgh_job_analyze(wcgh_job* job);
 int wcgh_job_download(wcgh_job* job, float* out);
 /* Stage snapshots of the last run (LUT method): base_LLL, after_LL,
  * after_L, after_full (synthesis.hpp:43-54), each rows x Nh complex64. */

@@ -83,6 +83,7 @@ _SIGS = [
     ("wcgh_job_upload", C.c_int, [_VP, _VP, _VP]),
     ("wcgh_job_upload_dev", C.c_int, [_VP, _VP, _VP]),
     ("wcgh_job_run", C.c_int, [_VP]),
+    ("wcgh_job_analyze", C.c_int, [_VP]),
     ("wcgh_job_download", C.c_int, [_VP, _VP]),
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),
     ("wcgh_job_plane_dev", _VP, [_VP]),

@@ -654,7 +654,7 @@ void finish_stats(wcgh_job* j, const unsigned long long* ops) {
   }
 }
 
-void run_job_direct(wcgh_job* j, cudaStream_t s) {
+void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
   j->timing.reset();
@@ -684,6 +684,11 @@ void run_job_direct(wcgh_job* j, cudaStream_t s) {
   const int* hoff = reinterpret_cast<const int*>(j->h_offsets);
   for (int l = 0; l <= L; ++l) lb[l] = hoff[l];
   j->stats.n_points = lb[L];
+  if (!synth) {  // front end only (wcgh_job_analyze)
+    WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_analysis, j->ev[0], j->ev[1]));
+    j->stats.ms_total = j->stats.ms_analysis;
+    return;
+  }
   // geometry bound on |dx|, |dy| for the phase-series plan
   const double far = double(j->off + No - 1);
   const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
@@ -724,7 +729,7 @@ __global__ void k_sum_stages(const float2* __restrict__ planes, size_t count, in
   out[i] = make_float2(re, im);
 }
 
-void run_job_lut(wcgh_job* j, cudaStream_t s) {
+void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
   j->timing.reset();
@@ -750,6 +755,14 @@ void run_job_lut(wcgh_job* j, cudaStream_t s) {
   sync(s);
   check_analysis_flags(*j->h_err);
   finish_stats(j, j->h_ops);
+  if (!synth) {  // front end only (wcgh_job_analyze): nonzero gated cells
+    long long cells = 0;
+    for (int k = 0; k < 4 * L; ++k) cells += j->h_tot[3 * k + 2];
+    j->stats.n_points = cells;
+    WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_analysis, j->ev[0], j->ev[1]));
+    j->stats.ms_total = j->stats.ms_analysis;
+    return;
+  }
   const size_t band = size_t(d.rows) * d.plane_size;
   float2* sp = j->stage_planes.as<float2>();
   long long cells = 0;
@@ -795,9 +808,22 @@ int wcgh_job_run(wcgh_job* job) {
     use_device(job->ctx);
     job->stats = wcgh_stats{};
     if (job->desc.method == WCGH_METHOD_LUT)
-      run_job_lut(job, job->ctx->stream);
+      run_job_lut(job, job->ctx->stream, true);
     else  // direct and FFT share the analysis + compaction front end
-      run_job_direct(job, job->ctx->stream);
+      run_job_direct(job, job->ctx->stream, true);
+  });
+}
+
+int wcgh_job_analyze(wcgh_job* job) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job != nullptr, "job_analyze: NULL job");
+    require(job->uploaded, "job_analyze: inputs not uploaded");
+    use_device(job->ctx);
+    job->stats = wcgh_stats{};
+    if (job->desc.method == WCGH_METHOD_LUT)
+      run_job_lut(job, job->ctx->stream, false);
+    else
+      run_job_direct(job, job->ctx->stream, false);
   });
 }
 

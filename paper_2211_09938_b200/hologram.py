@@ -96,6 +96,11 @@ class HologramJob:
     def run(self) -> None:
         L.check(self.ctx.lib.wcgh_job_run(self.h))
 
+    def analyze(self) -> dict:
+        """Front end only (K1/K2): op counts, point / cell count, ms_analysis."""
+        L.check(self.ctx.lib.wcgh_job_analyze(self.h))
+        return self.stats()
+
     def download(self, out: np.ndarray | None = None) -> np.ndarray:
         n = self.spec.plane_size
         if out is None:
