@@ -217,6 +217,12 @@ int wcgh_job_run(wcgh_job* job);
  * cells for the LUT method) and ms_analysis; no synthesis. */
 int wcgh_job_analyze(wcgh_job* job);
 int wcgh_job_download(wcgh_job* job, float* out);
+/* A_eff of the last run or analyze (n_layers x No^2 fp32, row-major). */
+int wcgh_job_download_a_eff(wcgh_job* job, float* out);
+/* Compacted point list of the last direct-method run or analyze (row-major
+ * ascending per layer): *n_out = count; copies it when out != NULL and
+ * capacity >= count. */
+int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, int64_t* n_out);
 /* Stage snapshots of the last run (LUT method): base_LLL, after_LL,
  * after_L, after_full (synthesis.hpp:43-54), each rows x Nh complex64. */
 int wcgh_job_download_stages(wcgh_job* job, float* out4);

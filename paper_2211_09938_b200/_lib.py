@@ -85,6 +85,8 @@ _SIGS = [
     ("wcgh_job_run", C.c_int, [_VP]),
     ("wcgh_job_analyze", C.c_int, [_VP]),
     ("wcgh_job_download", C.c_int, [_VP, _VP]),
+    ("wcgh_job_download_a_eff", C.c_int, [_VP, _VP]),
+    ("wcgh_job_download_points", C.c_int, [_VP, _VP, C.c_int64, C.POINTER(C.c_int64)]),
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),
     ("wcgh_job_plane_dev", _VP, [_VP]),
     ("wcgh_job_stats", C.c_int, [_VP, C.POINTER(Stats)]),

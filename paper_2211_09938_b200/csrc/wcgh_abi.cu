@@ -57,7 +57,7 @@ struct wcgh_ctx {
   DirectScratch direct;
   StageCells cells;
   ReconPlan recon;  // reconstruction / FFT entry points
-  DevBuf b_ssim;
+  DevBuf b_ssim, b_scan;
   std::mutex mu;
 };
 
@@ -67,7 +67,7 @@ struct wcgh_job {
   std::vector<wcgh_layer> layers;
   int off = 0;
   size_t in_elems = 0;  // per layer No^2
-  DevBuf obj, sal, a_eff, seg_counts, seg_offsets, ops, err, points, plane;
+  DevBuf obj, sal, a_eff, seg_counts, seg_offsets, scan_scratch, ops, err, points, plane;
   // LUT method
   DevBuf w_stage, stage_planes, lut_scratch, lut_partial;
   std::vector<std::unique_ptr<StageCells>> cells;  // [layer * 4 + stage]
@@ -346,7 +346,7 @@ int wcgh_analyze(wcgh_ctx* ctx, const void* object, int obj_dtype, double obj_sc
     ao.err = reinterpret_cast<int*>(ops + WCGH_OP_LEVELS);
     WCGH_CUDA(cudaMemsetAsync(ops, 0, 64, s));
     launch_analysis(in, obj_dtype, obj_scale, in + n2 * os, sal_dtype, n, 1, *plan, ao, s);
-    launch_scan(ao.seg_counts, seg_off, int(nseg), s);
+    launch_scan(ao.seg_counts, seg_off, int(nseg), s, &ctx->b_scan);
     unsigned long long h_ops[WCGH_OP_LEVELS];
     int flags = 0, total = 0;
     WCGH_CUDA(cudaMemcpyAsync(h_ops, ops, sizeof(h_ops), cudaMemcpyDeviceToHost, s));
@@ -378,7 +378,7 @@ int wcgh_analyze(wcgh_ctx* ctx, const void* object, int obj_dtype, double obj_sc
         int* ofs = cnt + nsg + 1;
         // b_misc was possibly reallocated: ops already copied out above
         launch_mask_counts(ao.masks + mofs[st], m, cnt, s);
-        launch_scan(cnt, ofs, int(nsg), s);
+        launch_scan(cnt, ofs, int(nsg), s, &ctx->b_scan);
         int c = 0;
         WCGH_CUDA(cudaMemcpyAsync(&c, ofs + nsg, sizeof(int), cudaMemcpyDeviceToHost, s));
         sync(s);
@@ -663,11 +663,12 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
   const size_t per_layer = size_t(No) * seg_per_row(No);
   const size_t nseg = per_layer * L;
   const bool fft = d.method == WCGH_METHOD_FFT;
-  launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s);
+  const int scan_launches = launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s,
+                                        &j->scan_scratch);
   if (!fft)
     launch_compact_points(j->a_eff.as<float>(), j->seg_offsets.as<int>(), No, L, j->off, 0,
                           j->points.as<wcgh_point>(), s);
-  j->stats.total_launches += fft ? 1 : 2;
+  j->stats.total_launches += scan_launches + (fft ? 0 : 1);
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
   // layer boundaries of the compacted list, ops and validation flags
   for (int l = 0; l <= L; ++l) {
@@ -833,6 +834,33 @@ int wcgh_job_download(wcgh_job* job, float* out) {
     use_device(job->ctx);
     cudaStream_t s = job->ctx->stream;
     WCGH_CUDA(cudaMemcpyAsync(out, job->plane.p, sizeof(float2) * size_t(job->desc.rows) * job->desc.plane_size, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_job_download_a_eff(wcgh_job* job, float* out) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && out, "job_download_a_eff: NULL argument");
+    use_device(job->ctx);
+    cudaStream_t s = job->ctx->stream;
+    WCGH_CUDA(cudaMemcpyAsync(out, job->a_eff.p, sizeof(float) * job->in_elems * job->desc.n_layers,
+                              cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, int64_t* n_out) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job != nullptr, "job_download_points: NULL job");
+    require(job->desc.method != WCGH_METHOD_LUT && job->desc.method != WCGH_METHOD_FFT,
+            "job_download_points: the compacted point list is built by the direct method");
+    const int64_t n = int64_t(job->stats.n_points);
+    if (n_out) *n_out = n;
+    if (out == nullptr) return;
+    require(capacity >= n, "job_download_points: capacity below the point count");
+    use_device(job->ctx);
+    cudaStream_t s = job->ctx->stream;
+    WCGH_CUDA(cudaMemcpyAsync(out, job->points.p, sizeof(wcgh_point) * size_t(n), cudaMemcpyDeviceToHost, s));
     sync(s);
   });
 }

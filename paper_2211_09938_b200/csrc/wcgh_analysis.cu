@@ -322,15 +322,68 @@ __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ counts, i
   if (threadIdx.x == 0) offsets[count] = carry;
 }
 
+// Multi-CTA exclusive scan for long count arrays: per-CTA scans of 4096
+// elements (4 consecutive per thread) with block totals in aux, a single-CTA
+// scan of the totals, then the block prefixes are added back.
+__global__ void __launch_bounds__(1024) k_scan_partial(const int* __restrict__ counts,
+                                                       int* __restrict__ offsets, int count,
+                                                       int* __restrict__ aux) {
+  __shared__ int warp_sums[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long i0 = (long long)blockIdx.x * 4096 + 4 * threadIdx.x;
+  int v[4], t = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = i0 + k < count ? counts[i0 + k] : 0;
+    t += v[k];
+  }
+  int x = t;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_sums[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int run = x - t + (warp ? warp_sums[warp - 1] : 0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (i0 + k < count) offsets[i0 + k] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 1023) aux[blockIdx.x] = run;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_add(int* __restrict__ offsets, int count,
+                                                   const int* __restrict__ aux_ofs, int nb) {
+  const long long i0 = (long long)blockIdx.x * 4096 + 4 * threadIdx.x;
+  const int add = aux_ofs[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (i0 + k < count) offsets[i0 + k] += add;
+  if (blockIdx.x == 0 && threadIdx.x == 0) offsets[count] = aux_ofs[nb];
+}
+
 // Ordered compaction: one warp per (layer, row, 128-pixel segment); lane l
-// owns pixels 4l..4l+3 of the segment.
+// owns pixels 4l..4l+3 of the segment (one float4 load). The segment's point
+// records are assembled in shared memory and written as one contiguous,
+// coalesced run of 16-byte stores.
 __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict__ a_eff,
                                                         const int* __restrict__ offsets, int n,
                                                         int n_layers, int off, int layer0,
                                                         wcgh_point* __restrict__ points) {
-  const int lane = threadIdx.x & 31;
+  __shared__ int4 stage[8][128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int segs = seg_per_row(n);
-  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const long long gw = (long long)blockIdx.x * 8 + warp;
   const long long total = (long long)n_layers * n * segs;
   if (gw >= total) return;
   const int seg = int(gw % segs);
@@ -340,29 +393,31 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
   const float* src = a_eff + (size_t(layer) * n + row) * n;
   const int x0 = seg * 128 + 4 * lane;
   float v[4];
+  if (x0 + 3 < n && (n & 3) == 0) {
+    const float4 f = *reinterpret_cast<const float4*>(src + x0);
+    v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = (x0 + k < n) ? src[x0 + k] : 0.0f;
+  }
   int nz = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    v[k] = (x0 + k < n) ? src[x0 + k] : 0.0f;
-    nz += v[k] != 0.0f;
-  }
+  for (int k = 0; k < 4; ++k) nz += v[k] != 0.0f;
   int incl = nz;
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += y;
   }
-  int pos = offsets[gw] + incl - nz;
+  const int seg_total = __shfl_sync(kFull, incl, 31);
+  int pos = incl - nz;
+  const int py = row + off, pl = layer0 + layer;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (v[k] != 0.0f) {
-      wcgh_point p;
-      p.x = x0 + k + off;
-      p.y = row + off;
-      p.a = v[k];
-      p.layer = layer0 + layer;
-      points[pos++] = p;
-    }
+    if (v[k] != 0.0f) stage[warp][pos++] = make_int4(x0 + k + off, py, __float_as_int(v[k]), pl);
   }
+  __syncwarp();
+  int4* dst = reinterpret_cast<int4*>(points) + offsets[gw];
+  for (int i = lane; i < seg_total; i += 32) dst[i] = stage[warp][i];
 }
 
 // Mask cell lists (row-major ascending y*m + x), same two-pass scheme.
@@ -467,6 +522,190 @@ __global__ void k_expand_residual(const double* __restrict__ h, const double* __
       out[size_t(2 * y + sy) * n + 2 * x + sx] = expand_at(h[i], v[i], d[i], sx, sy);
 }
 
+// ---- K1 fast path: uint8 object (scale 1) and uint8 saliency, no
+// validation dumps (the job's production inputs). Integer inputs make every
+// band a dyadic rational with a small numerator, so the reference's fp64
+// arithmetic is exact and an integer restatement is bit-identical. With
+// S1 = 4 a1 (level-1 quad sums), S2 = 16 a2, S3 = 64 a3, the expanded
+// residuals are the child minus the parent mean (synthesize_level with
+// a = 0 applied to the analysis of the same block, haar.cpp:12-48):
+//   R1 = 4 r_full = 4 c - S1,  R2 = 16 r_l = 4 S1 - S2,  R3 = 64 r_ll = 4 S2 - S3,
+// and 64 A_eff = S3 + g_ll R3 + 4 g_l R2 + 16 g_full R1 is an exact int32,
+// so A_eff = float(E) / 64 equals the fp64 value rounded to fp32. Gates
+// compare u8 block maxima with integer cut-offs cut(t) = min{v : v * (1/255.0)
+// > t}, computed on the host with load_sal's fp64 expression.
+// Thread mapping: one thread per 8 x 8 LLL cell (all three levels in
+// registers, no shuffles), 8-byte coalesced row loads and float4 A_eff stores
+// (a warp covers 256 x 8 pixels); per-(row, 128-px segment) nonzero counts by
+// packed half-warp reductions. Memory-bound: 1 B + 1 B read, 4 B written per
+// pixel.
+struct U8Cuts {
+  int ll, l, full;  // 256 = stage disabled / never open
+};
+
+__device__ __forceinline__ int byte_at(uint2 w, int k) {
+  return int(((k < 4 ? w.x : w.y) >> (8 * (k & 3))) & 0xffu);
+}
+
+constexpr int kU8Threads = 128;  // 128 LLL cells = 1024 pixels per CTA row strip
+
+__global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __restrict__ obj,
+                                                              const uint8_t* __restrict__ sal,
+                                                              int n, U8Cuts cut, AnalysisOut out) {
+  const int lane = threadIdx.x & 31;
+  const int layer = blockIdx.z;
+  const size_t n2 = size_t(n) * n;
+  const int m3 = n / 8, m2 = n / 4, m1 = n / 2;
+  const int bx = blockIdx.x * kU8Threads + threadIdx.x;  // LLL cell column
+  const int by = blockIdx.y;                              // LLL cell row
+  const bool valid = bx < m3;
+  const int X0 = 8 * bx, Y0 = 8 * by;
+  obj += layer * n2;
+  sal += layer * n2;
+
+  uint2 ov[8], sv[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    ov[r] = valid ? *reinterpret_cast<const uint2*>(obj + size_t(Y0 + r) * n + X0) : make_uint2(0, 0);
+    sv[r] = valid ? *reinterpret_cast<const uint2*>(sal + size_t(Y0 + r) * n + X0) : make_uint2(0, 0);
+  }
+
+  // level 1: quad sums and saliency maxima (4 x 4 quads)
+  int S1[4][4], M1[4][4];
+#pragma unroll
+  for (int qy = 0; qy < 4; ++qy)
+#pragma unroll
+    for (int qx = 0; qx < 4; ++qx) {
+      S1[qy][qx] = byte_at(ov[2 * qy], 2 * qx) + byte_at(ov[2 * qy], 2 * qx + 1) +
+                   byte_at(ov[2 * qy + 1], 2 * qx) + byte_at(ov[2 * qy + 1], 2 * qx + 1);
+      M1[qy][qx] = max(max(byte_at(sv[2 * qy], 2 * qx), byte_at(sv[2 * qy], 2 * qx + 1)),
+                       max(byte_at(sv[2 * qy + 1], 2 * qx), byte_at(sv[2 * qy + 1], 2 * qx + 1)));
+    }
+  // level 2 (2 x 2 cells) and level 3 (the LLL cell)
+  int S2[2][2];
+  bool G2[2][2];
+#pragma unroll
+  for (int uy = 0; uy < 2; ++uy)
+#pragma unroll
+    for (int ux = 0; ux < 2; ++ux) {
+      S2[uy][ux] = S1[2 * uy][2 * ux] + S1[2 * uy][2 * ux + 1] + S1[2 * uy + 1][2 * ux] +
+                   S1[2 * uy + 1][2 * ux + 1];
+      G2[uy][ux] = max(max(M1[2 * uy][2 * ux], M1[2 * uy][2 * ux + 1]),
+                       max(M1[2 * uy + 1][2 * ux], M1[2 * uy + 1][2 * ux + 1])) >= cut.ll;
+    }
+  const int S3 = S2[0][0] + S2[0][1] + S2[1][0] + S2[1][1];
+
+  // per level-1 quad: 64 (a3 + g_ll r_ll + g_l r_l)
+  int Eq[4][4];
+  int n_l = 0, n_f = 0;
+#pragma unroll
+  for (int qy = 0; qy < 4; ++qy)
+#pragma unroll
+    for (int qx = 0; qx < 4; ++qx) {
+      const int ux = qx >> 1, uy = qy >> 1;
+      int e = S3;
+      if (G2[uy][ux]) e += 4 * S2[uy][ux] - S3;
+      const bool gl = M1[qy][qx] >= cut.l;
+      n_l += gl;
+      if (gl) e += 4 * (4 * S1[qy][qx] - S2[uy][ux]);
+      Eq[qy][qx] = e;
+    }
+
+  float* ae = out.a_eff + layer * n2;
+  float* wf = out.w_stage ? out.w_stage + layer * wstage_len(n) + size_t(m3) * m3 +
+                                size_t(m2) * m2 + size_t(m1) * m1
+                          : nullptr;
+  unsigned cnt_lo = 0, cnt_hi = 0;  // nonzero A_eff per row, 8 bits per row
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    float a[8];
+    int nz = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int qy = r >> 1, qx = c >> 1;
+      const bool gf = byte_at(sv[r], c) >= cut.full;
+      n_f += gf;
+      const int r1 = 4 * byte_at(ov[r], c) - S1[qy][qx];
+      const int e = Eq[qy][qx] + (gf ? 16 * r1 : 0);
+      a[c] = float(e) * (1.0f / 64.0f);
+      nz += e != 0;
+      if (wf && valid) wf[size_t(Y0 + r) * n + X0 + c] = gf ? float(r1) * 0.25f : 0.0f;
+    }
+    if (r < 4) cnt_lo |= unsigned(nz) << (8 * r);
+    else cnt_hi |= unsigned(nz) << (8 * (r - 4));
+    if (valid) {
+      float4* dst = reinterpret_cast<float4*>(ae + size_t(Y0 + r) * n + X0);
+      dst[0] = make_float4(a[0], a[1], a[2], a[3]);
+      dst[1] = make_float4(a[4], a[5], a[6], a[7]);
+    }
+  }
+  if (!valid) n_l = n_f = 0;
+
+  if (out.w_stage && valid) {
+    float* w = out.w_stage + layer * wstage_len(n);
+    float* w_ll = w + size_t(m3) * m3;
+    float* w_l = w_ll + size_t(m2) * m2;
+    w[size_t(by) * m3 + bx] = float(S3) * (1.0f / 64.0f);
+#pragma unroll
+    for (int uy = 0; uy < 2; ++uy)
+#pragma unroll
+      for (int ux = 0; ux < 2; ++ux)
+        w_ll[size_t(2 * by + uy) * m2 + 2 * bx + ux] =
+            G2[uy][ux] ? float(4 * S2[uy][ux] - S3) * (1.0f / 64.0f) : 0.0f;
+#pragma unroll
+    for (int qy = 0; qy < 4; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < 4; ++qx)
+        w_l[size_t(4 * by + qy) * m1 + 4 * bx + qx] =
+            M1[qy][qx] >= cut.l ? float(4 * S1[qy][qx] - S2[qy >> 1][qx >> 1]) * (1.0f / 16.0f)
+                                : 0.0f;
+  }
+
+  // operator counts (synthesis.cpp:68, 77-88): every LLL cell, gated cells
+  int n_ll = valid ? int(G2[0][0]) + int(G2[0][1]) + int(G2[1][0]) + int(G2[1][1]) : 0;
+  int n_b = valid ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    n_b += __shfl_xor_sync(kFull, n_b, o);
+    n_ll += __shfl_xor_sync(kFull, n_ll, o);
+    n_l += __shfl_xor_sync(kFull, n_l, o);
+    n_f += __shfl_xor_sync(kFull, n_f, o);
+  }
+  if (lane == 0 && n_b) {
+    unsigned long long* ops = out.ops + layer * WCGH_OP_LEVELS;
+    atomicAdd(ops + WCGH_OP_BASE_LLL, (unsigned long long)n_b);
+    if (n_ll) atomicAdd(ops + WCGH_OP_REFINE_LL, (unsigned long long)n_ll);
+    if (n_l) atomicAdd(ops + WCGH_OP_REFINE_L, (unsigned long long)n_l);
+    if (n_f) atomicAdd(ops + WCGH_OP_REFINE_FULL, (unsigned long long)n_f);
+  }
+
+  // nonzero counts per (row, 128-pixel segment) = 16 consecutive cells
+  if (out.seg_counts) {
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      cnt_lo += __shfl_xor_sync(kFull, cnt_lo, o);
+      cnt_hi += __shfl_xor_sync(kFull, cnt_hi, o);
+    }
+    if ((lane & 15) == 0 && valid) {
+      const int segs = seg_per_row(n);
+      const int seg = X0 / 128;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const unsigned v = ((r < 4 ? cnt_lo : cnt_hi) >> (8 * (r & 3))) & 0xffu;
+        out.seg_counts[(size_t(layer) * n + Y0 + r) * segs + seg] = int(v);
+      }
+    }
+  }
+}
+
+// smallest u8 value v with v * (1/255) > t in fp64 (load_sal's expression)
+int u8_cut(double t, int enabled) {
+  if (!enabled) return 256;
+  for (int v = 0; v < 256; ++v)
+    if (double(v) * (1.0 / 255.0) > t) return v;
+  return 256;
+}
+
 template <typename TO, typename TS>
 void launch_k1(const void* obj, double scale, const void* sal, int n, int n_layers,
                const wcgh_plan& plan, const AnalysisOut& out, cudaStream_t s) {
@@ -492,6 +731,16 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
                     int sal_dtype, int n, int n_layers, const wcgh_plan& plan,
                     const AnalysisOut& out, cudaStream_t s) {
   require(n >= 8 && n % 8 == 0, "analysis: side must be a positive multiple of 8");
+  if (obj_dtype == WCGH_U8 && sal_dtype == WCGH_U8 && obj_scale == 1.0 && !out.pyramid &&
+      !out.sal_pyr && !out.masks) {
+    const U8Cuts cut{u8_cut(plan.t_ll, plan.enable_ll), u8_cut(plan.t_l, plan.enable_l),
+                     u8_cut(plan.t_full, plan.enable_full)};
+    dim3 grid(unsigned((n / 8 + kU8Threads - 1) / kU8Threads), unsigned(n / 8), unsigned(n_layers));
+    k_analysis_u8<<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
+                                               static_cast<const uint8_t*>(sal), n, cut, out);
+    WCGH_CHECK_LAUNCH();
+    return 1;
+  }
   switch (obj_dtype) {
     case WCGH_U8: dispatch_sal<uint8_t>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
     case WCGH_F32: dispatch_sal<float>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
@@ -502,10 +751,23 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
   return 1;
 }
 
-int launch_scan(const int* counts, int* offsets, int count, cudaStream_t s) {
-  k_scan<<<1, 1024, 0, s>>>(counts, offsets, count);
+int launch_scan(const int* counts, int* offsets, int count, cudaStream_t s, DevBuf* scratch) {
+  constexpr int kSingle = 1 << 16;  // one CTA is fastest (one launch) below this
+  if (count <= kSingle || scratch == nullptr) {
+    k_scan<<<1, 1024, 0, s>>>(counts, offsets, count);
+    WCGH_CHECK_LAUNCH();
+    return 1;
+  }
+  const int nb = (count + 4095) / 4096;
+  int* aux = static_cast<int*>(scratch->reserve(sizeof(int) * (2 * size_t(nb) + 1)));
+  int* aux_ofs = aux + nb;
+  k_scan_partial<<<nb, 1024, 0, s>>>(counts, offsets, count, aux);
   WCGH_CHECK_LAUNCH();
-  return 1;
+  k_scan<<<1, 1024, 0, s>>>(aux, aux_ofs, nb);
+  WCGH_CHECK_LAUNCH();
+  k_scan_add<<<nb, 1024, 0, s>>>(offsets, count, aux_ofs, nb);
+  WCGH_CHECK_LAUNCH();
+  return 3;
 }
 
 int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers, int off,

@@ -178,7 +178,10 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
                     int sal_dtype, int n, int n_layers, const wcgh_plan& plan,
                     const AnalysisOut& out, cudaStream_t stream);
 // Exclusive scan of `count` ints into `offsets` (count + 1 entries, last = total).
-int launch_scan(const int* counts, int* offsets, int count, cudaStream_t stream);
+// Exclusive scan, offsets[count] = total. With `scratch`, long arrays use a
+// multi-CTA scan (3 launches); otherwise one CTA.
+int launch_scan(const int* counts, int* offsets, int count, cudaStream_t stream,
+                DevBuf* scratch = nullptr);
 // Ordered compaction of nonzero A_eff into points (hologram coordinates).
 int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers,
                           int offset, int layer0, wcgh_point* points, cudaStream_t stream);

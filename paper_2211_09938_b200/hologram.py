@@ -109,6 +109,21 @@ class HologramJob:
         L.check(self.ctx.lib.wcgh_job_download(self.h, L.ptr(out)))
         return out
 
+    def download_a_eff(self) -> np.ndarray:
+        """A_eff of the last run/analyze, (n_layers, No, No) fp32."""
+        no = self.spec.object_size
+        out = np.empty((len(self.spec.layers), no, no), np.float32)
+        L.check(self.ctx.lib.wcgh_job_download_a_eff(self.h, L.ptr(out)))
+        return out
+
+    def download_points(self) -> np.ndarray:
+        """Compacted point records of the last direct-method run/analyze."""
+        n = C.c_int64(0)
+        L.check(self.ctx.lib.wcgh_job_download_points(self.h, None, 0, C.byref(n)))
+        out = np.empty(n.value, L.POINT_DTYPE)
+        L.check(self.ctx.lib.wcgh_job_download_points(self.h, L.ptr(out), n.value, C.byref(n)))
+        return out
+
     def download_stages(self) -> np.ndarray:
         n = self.spec.plane_size
         out = np.empty((4, self.rows, n), np.complex64)
