@@ -549,27 +549,15 @@ __device__ __forceinline__ int byte_at(uint2 w, int k) {
 
 constexpr int kU8Threads = 128;  // 128 LLL cells = 1024 pixels per CTA row strip
 
-__global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __restrict__ obj,
-                                                              const uint8_t* __restrict__ sal,
-                                                              int n, U8Cuts cut, AnalysisOut out) {
+// One LLL cell (8 x 8 pixels at X0 = 8 bx, Y0 = 8 by) from its loaded rows.
+template <bool WSTAGE>
+__device__ __forceinline__ void cell_u8(const uint2 (&ov)[8], const uint2 (&sv)[8], int bx, int by,
+                                        bool valid, int n, int layer, const U8Cuts& cut,
+                                        const AnalysisOut& out) {
   const int lane = threadIdx.x & 31;
-  const int layer = blockIdx.z;
   const size_t n2 = size_t(n) * n;
   const int m3 = n / 8, m2 = n / 4, m1 = n / 2;
-  const int bx = blockIdx.x * kU8Threads + threadIdx.x;  // LLL cell column
-  const int by = blockIdx.y;                              // LLL cell row
-  const bool valid = bx < m3;
   const int X0 = 8 * bx, Y0 = 8 * by;
-  obj += layer * n2;
-  sal += layer * n2;
-
-  uint2 ov[8], sv[8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    ov[r] = valid ? *reinterpret_cast<const uint2*>(obj + size_t(Y0 + r) * n + X0) : make_uint2(0, 0);
-    sv[r] = valid ? *reinterpret_cast<const uint2*>(sal + size_t(Y0 + r) * n + X0) : make_uint2(0, 0);
-  }
-
   // level 1: quad sums and saliency maxima (4 x 4 quads)
   int S1[4][4], M1[4][4];
 #pragma unroll
@@ -612,9 +600,9 @@ __global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __
     }
 
   float* ae = out.a_eff + layer * n2;
-  float* wf = out.w_stage ? out.w_stage + layer * wstage_len(n) + size_t(m3) * m3 +
-                                size_t(m2) * m2 + size_t(m1) * m1
-                          : nullptr;
+  float* wf = WSTAGE ? out.w_stage + layer * wstage_len(n) + size_t(m3) * m3 +
+                           size_t(m2) * m2 + size_t(m1) * m1
+                     : nullptr;
   unsigned cnt_lo = 0, cnt_hi = 0;  // nonzero A_eff per row, 8 bits per row
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
@@ -629,7 +617,7 @@ __global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __
       const int e = Eq[qy][qx] + (gf ? 16 * r1 : 0);
       a[c] = float(e) * (1.0f / 64.0f);
       nz += e != 0;
-      if (wf && valid) wf[size_t(Y0 + r) * n + X0 + c] = gf ? float(r1) * 0.25f : 0.0f;
+      if (WSTAGE && valid) wf[size_t(Y0 + r) * n + X0 + c] = gf ? float(r1) * 0.25f : 0.0f;
     }
     if (r < 4) cnt_lo |= unsigned(nz) << (8 * r);
     else cnt_hi |= unsigned(nz) << (8 * (r - 4));
@@ -641,7 +629,7 @@ __global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __
   }
   if (!valid) n_l = n_f = 0;
 
-  if (out.w_stage && valid) {
+  if (WSTAGE && valid) {
     float* w = out.w_stage + layer * wstage_len(n);
     float* w_ll = w + size_t(m3) * m3;
     float* w_l = w_ll + size_t(m2) * m2;
@@ -698,6 +686,35 @@ __global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __
   }
 }
 
+// Two vertically adjacent cells per thread: both cells' rows are loaded
+// before either is computed, so 256 B per thread are in flight.
+template <bool WSTAGE>
+__global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __restrict__ obj,
+                                                              const uint8_t* __restrict__ sal,
+                                                              int n, U8Cuts cut, AnalysisOut out) {
+  const int layer = blockIdx.z;
+  const size_t n2 = size_t(n) * n;
+  const int m3 = n / 8;
+  const int bx = blockIdx.x * kU8Threads + threadIdx.x;  // LLL cell column
+  const int by0 = 2 * blockIdx.y;                         // first LLL cell row
+  const bool valid0 = bx < m3, valid1 = valid0 && by0 + 1 < m3;
+  obj += layer * n2;
+  sal += layer * n2;
+  uint2 ov[2][8], sv[2][8];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool v = k ? valid1 : valid0;
+    const size_t base = size_t(8 * (by0 + k)) * n + 8 * bx;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      ov[k][r] = v ? *reinterpret_cast<const uint2*>(obj + base + size_t(r) * n) : make_uint2(0, 0);
+      sv[k][r] = v ? *reinterpret_cast<const uint2*>(sal + base + size_t(r) * n) : make_uint2(0, 0);
+    }
+  }
+  cell_u8<WSTAGE>(ov[0], sv[0], bx, by0, valid0, n, layer, cut, out);
+  if (by0 + 1 < m3) cell_u8<WSTAGE>(ov[1], sv[1], bx, by0 + 1, valid1, n, layer, cut, out);
+}
+
 // smallest u8 value v with v * (1/255) > t in fp64 (load_sal's expression)
 int u8_cut(double t, int enabled) {
   if (!enabled) return 256;
@@ -735,9 +752,14 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
       !out.sal_pyr && !out.masks) {
     const U8Cuts cut{u8_cut(plan.t_ll, plan.enable_ll), u8_cut(plan.t_l, plan.enable_l),
                      u8_cut(plan.t_full, plan.enable_full)};
-    dim3 grid(unsigned((n / 8 + kU8Threads - 1) / kU8Threads), unsigned(n / 8), unsigned(n_layers));
-    k_analysis_u8<<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
-                                               static_cast<const uint8_t*>(sal), n, cut, out);
+    dim3 grid(unsigned((n / 8 + kU8Threads - 1) / kU8Threads), unsigned((n / 8 + 1) / 2),
+              unsigned(n_layers));
+    if (out.w_stage)
+      k_analysis_u8<true><<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
+                                                      static_cast<const uint8_t*>(sal), n, cut, out);
+    else
+      k_analysis_u8<false><<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
+                                                       static_cast<const uint8_t*>(sal), n, cut, out);
     WCGH_CHECK_LAUNCH();
     return 1;
   }
