@@ -686,24 +686,23 @@ __device__ __forceinline__ void cell_u8(const uint2 (&ov)[8], const uint2 (&sv)[
   }
 }
 
-// Two vertically adjacent cells per thread: both cells' rows are loaded
-// before either is computed, so 256 B per thread are in flight.
-template <bool WSTAGE>
-__global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __restrict__ obj,
-                                                              const uint8_t* __restrict__ sal,
-                                                              int n, U8Cuts cut, AnalysisOut out) {
+// CELLS vertically adjacent cells per thread: all their rows are loaded
+// before any is computed (CELLS x 128 B in flight per thread).
+template <bool WSTAGE, int CELLS, int MINB>
+__global__ void __launch_bounds__(kU8Threads, MINB) k_analysis_u8(const uint8_t* __restrict__ obj,
+                                                                 const uint8_t* __restrict__ sal,
+                                                                 int n, U8Cuts cut, AnalysisOut out) {
   const int layer = blockIdx.z;
   const size_t n2 = size_t(n) * n;
   const int m3 = n / 8;
   const int bx = blockIdx.x * kU8Threads + threadIdx.x;  // LLL cell column
-  const int by0 = 2 * blockIdx.y;                         // first LLL cell row
-  const bool valid0 = bx < m3, valid1 = valid0 && by0 + 1 < m3;
+  const int by0 = CELLS * blockIdx.y;                     // first LLL cell row
   obj += layer * n2;
   sal += layer * n2;
-  uint2 ov[2][8], sv[2][8];
+  uint2 ov[CELLS][8], sv[CELLS][8];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool v = k ? valid1 : valid0;
+  for (int k = 0; k < CELLS; ++k) {
+    const bool v = bx < m3 && by0 + k < m3;
     const size_t base = size_t(8 * (by0 + k)) * n + 8 * bx;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -711,8 +710,19 @@ __global__ void __launch_bounds__(kU8Threads, 3) k_analysis_u8(const uint8_t* __
       sv[k][r] = v ? *reinterpret_cast<const uint2*>(sal + base + size_t(r) * n) : make_uint2(0, 0);
     }
   }
-  cell_u8<WSTAGE>(ov[0], sv[0], bx, by0, valid0, n, layer, cut, out);
-  if (by0 + 1 < m3) cell_u8<WSTAGE>(ov[1], sv[1], bx, by0 + 1, valid1, n, layer, cut, out);
+#pragma unroll
+  for (int k = 0; k < CELLS; ++k)
+    if (by0 + k < m3) cell_u8<WSTAGE>(ov[k], sv[k], bx, by0 + k, bx < m3, n, layer, cut, out);
+}
+
+template <bool WSTAGE>
+void launch_u8(const void* obj, const void* sal, int n, int n_layers, const U8Cuts& cut,
+               const AnalysisOut& out, cudaStream_t s) {
+  constexpr int kCells = 1;
+  dim3 grid(unsigned((n / 8 + kU8Threads - 1) / kU8Threads), unsigned((n / 8 + kCells - 1) / kCells),
+            unsigned(n_layers));
+  k_analysis_u8<WSTAGE, kCells, 4><<<grid, kU8Threads, 0, s>>>(
+      static_cast<const uint8_t*>(obj), static_cast<const uint8_t*>(sal), n, cut, out);
 }
 
 // smallest u8 value v with v * (1/255) > t in fp64 (load_sal's expression)
@@ -752,14 +762,10 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
       !out.sal_pyr && !out.masks) {
     const U8Cuts cut{u8_cut(plan.t_ll, plan.enable_ll), u8_cut(plan.t_l, plan.enable_l),
                      u8_cut(plan.t_full, plan.enable_full)};
-    dim3 grid(unsigned((n / 8 + kU8Threads - 1) / kU8Threads), unsigned((n / 8 + 1) / 2),
-              unsigned(n_layers));
     if (out.w_stage)
-      k_analysis_u8<true><<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
-                                                      static_cast<const uint8_t*>(sal), n, cut, out);
+      launch_u8<true>(obj, sal, n, n_layers, cut, out, s);
     else
-      k_analysis_u8<false><<<grid, kU8Threads, 0, s>>>(static_cast<const uint8_t*>(obj),
-                                                       static_cast<const uint8_t*>(sal), n, cut, out);
+      launch_u8<false>(obj, sal, n, n_layers, cut, out, s);
     WCGH_CHECK_LAUNCH();
     return 1;
   }
