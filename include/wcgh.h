@@ -223,8 +223,10 @@ int wcgh_job_download_a_eff(wcgh_job* job, float* out);
  * ascending per layer): *n_out = count; copies it when out != NULL and
  * capacity >= count. */
 int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, int64_t* n_out);
-/* Stage snapshots of the last run (LUT method): base_LLL, after_LL,
- * after_L, after_full (synthesis.hpp:43-54), each rows x Nh complex64. */
+/* Stage snapshots of the last run: base_LLL, after_LL, after_L, after_full
+ * (synthesis.hpp:43-54), each rows x Nh complex64. The LUT method keeps its
+ * stage planes from the run; the direct and FFT methods synthesise the four
+ * per-stage amplitude deltas on demand (first call after a run). */
 int wcgh_job_download_stages(wcgh_job* job, float* out4);
 /* Device pointer of the row band (rows x Nh complex64), valid until destroy. */
 void* wcgh_job_plane_dev(wcgh_job* job);
@@ -240,9 +242,9 @@ int wcgh_write_cgh1(const char* path, const float* plane, int n, const wcgh_laye
  * payload into `plane` if it is non-NULL and capacity >= N^2 complex64. */
 int wcgh_read_cgh1(const char* path, float* plane, int64_t capacity, int* n_out,
                    wcgh_layer* scene_out);
-/* Writes the last run's full plane (stage < 0) or a LUT-method stage
- * snapshot (0..3 = base_LLL, after_LL, after_L, after_full) of a whole-plane
- * job (row0 = 0, rows = plane_size) as CGH1, scene = layer 0. */
+/* Writes the last run's full plane (stage < 0) or a stage snapshot
+ * (0..3 = base_LLL, after_LL, after_L, after_full) of a whole-plane job
+ * (row0 = 0, rows = plane_size) as CGH1, scene = layer 0. */
 int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage);
 
 /* ---- Reconstruction and metrics -------------------

@@ -84,6 +84,9 @@ struct wcgh_job {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   wcgh_stats stats{};
   bool uploaded = false;
+  bool ran = false;           // a run finished since the last upload
+  bool stages_ready = false;  // stage_planes hold the per-stage planes of the last run
+  DevBuf snap_img, snap_points;  // direct/FFT snapshots (computed on demand)
   ~wcgh_job() {
     if (h_tot) cudaFreeHost(h_tot);
     if (h_offsets) cudaFreeHost(h_offsets);
@@ -612,6 +615,7 @@ int wcgh_job_upload(wcgh_job* job, const void* object, const void* saliency) {
     WCGH_CUDA(cudaMemcpyAsync(job->obj.p, object, job->in_elems * L * dtype_size(job->desc.obj_dtype), cudaMemcpyHostToDevice, s));
     WCGH_CUDA(cudaMemcpyAsync(job->sal.p, saliency, job->in_elems * L * dtype_size(job->desc.sal_dtype), cudaMemcpyHostToDevice, s));
     job->uploaded = true;
+    job->ran = job->stages_ready = false;
   });
 }
 
@@ -624,6 +628,7 @@ int wcgh_job_upload_dev(wcgh_job* job, const void* object, const void* saliency)
     WCGH_CUDA(cudaMemcpyAsync(job->obj.p, object, job->in_elems * L * dtype_size(job->desc.obj_dtype), cudaMemcpyDeviceToDevice, s));
     WCGH_CUDA(cudaMemcpyAsync(job->sal.p, saliency, job->in_elems * L * dtype_size(job->desc.sal_dtype), cudaMemcpyDeviceToDevice, s));
     job->uploaded = true;
+    job->ran = job->stages_ready = false;
   });
 }
 
@@ -798,6 +803,51 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
   WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_total, j->ev[0], j->ev[3]));
 }
 
+// Stage snapshots of a direct- or FFT-method job (synthesis.hpp:43-54):
+// per-stage planes of the stage's amplitude contribution (base LLL, gated
+// LL, L, full residuals), synthesised by the job's own method; their prefix
+// sums are base_LLL, after_LL, after_L, after_full (linearity). Computed on
+// demand, outside wcgh_job_run.
+void compute_stage_planes(wcgh_job* j, cudaStream_t s) {
+  const wcgh_desc& d = j->desc;
+  const int No = d.object_size, L = d.n_layers;
+  const wcgh_stats keep = j->stats;
+  const size_t band = size_t(d.rows) * d.plane_size;
+  j->w_stage.reserve(sizeof(float) * wstage_len(No) * L);
+  float2* planes = static_cast<float2*>(j->stage_planes.reserve(sizeof(float2) * band * 4));
+  run_analysis(j, s, true);
+  float* img = static_cast<float*>(j->snap_img.reserve(sizeof(float) * j->in_elems * L));
+  const size_t per_layer = size_t(No) * seg_per_row(No);
+  const size_t nseg = per_layer * L;
+  const double far = double(j->off + No - 1);
+  const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
+                                 std::fabs(double(d.row0 + d.rows - 1) - j->off));
+  for (int st = 0; st < 4; ++st) {
+    launch_stage_delta(j->w_stage.as<float>(), No, L, st, img, s);
+    float2* out = planes + band * st;
+    if (d.method == WCGH_METHOD_FFT) {
+      launch_fft_synthesis(j->fft, img, No, j->off, d.plane_size, d.row0, d.rows, out, s, nullptr);
+      continue;
+    }
+    launch_seg_counts_f32(img, No, L, j->seg_counts.as<int>(), s);
+    launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s, &j->scan_scratch);
+    wcgh_point* pts = static_cast<wcgh_point*>(j->snap_points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1)));
+    launch_compact_points(img, j->seg_offsets.as<int>(), No, L, j->off, 0, pts, s);
+    for (int l = 0; l <= L; ++l)
+      WCGH_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(j->h_offsets) + l,
+                                j->seg_offsets.as<int>() + per_layer * size_t(l), sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+    sync(s);
+    int64_t lb[kMaxLayers + 1];
+    for (int l = 0; l <= L; ++l) lb[l] = reinterpret_cast<const int*>(j->h_offsets)[l];
+    launch_direct(pts, lb, L, d.layers, d.plane_size, d.row0, d.rows, d.phase_mode, far, max_dy,
+                  out, j->direct, s, nullptr, nullptr);
+  }
+  sync(s);
+  j->stats = keep;
+  j->stages_ready = true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -808,10 +858,13 @@ int wcgh_job_run(wcgh_job* job) {
     require(job->uploaded, "job_run: inputs not uploaded");
     use_device(job->ctx);
     job->stats = wcgh_stats{};
+    job->ran = job->stages_ready = false;
     if (job->desc.method == WCGH_METHOD_LUT)
       run_job_lut(job, job->ctx->stream, true);
     else  // direct and FFT share the analysis + compaction front end
       run_job_direct(job, job->ctx->stream, true);
+    job->ran = true;
+    job->stages_ready = job->desc.method == WCGH_METHOD_LUT;
   });
 }
 
@@ -868,10 +921,10 @@ int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, i
 int wcgh_job_download_stages(wcgh_job* job, float* out4) {
   return guard(job ? job->ctx : nullptr, [&] {
     require(job && out4, "job_download_stages: NULL argument");
-    require(job->desc.method == WCGH_METHOD_LUT,
-            "job_download_stages: stage snapshots are produced by the LUT method");
+    require(job->ran, "job_download_stages: run the job first");
     use_device(job->ctx);
     cudaStream_t s = job->ctx->stream;
+    if (!job->stages_ready) compute_stage_planes(job, s);
     const size_t band = size_t(job->desc.rows) * job->desc.plane_size;
     float2* tmp = static_cast<float2*>(job->lut_scratch.reserve(sizeof(float2) * band));
     for (int st = 0; st < 4; ++st) {

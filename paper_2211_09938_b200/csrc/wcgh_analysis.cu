@@ -420,6 +420,49 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
   for (int i = lane; i < seg_total; i += 32) dst[i] = stage[warp][i];
 }
 
+// Stage contribution images for the snapshots of the direct and FFT
+// methods (synthesis.hpp:43-54): stage s's per-pixel amplitude delta, the
+// stage weight of the pixel's cell (base: (No/8)^2 grid, block 8; LL: block
+// 4; L: block 2; full: block 1) from the dense w_stage grids. sum_s delta_s
+// == A_eff exactly for integer inputs (dyadic values, exact fp32 sums).
+__global__ void k_stage_delta(const float* __restrict__ w_stage, int n, int n_layers, int stage,
+                              float* __restrict__ out) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t n2 = size_t(n) * n;
+  if (i >= n2 * n_layers) return;
+  const int layer = int(i / n2);
+  const int x = int(i % n), y = int((i % n2) / n);
+  const int m3 = n / 8, m2 = n / 4, m1 = n / 2;
+  const float* w = w_stage + layer * wstage_len(n);
+  float v;
+  switch (stage) {
+    case 0: v = w[size_t(y / 8) * m3 + x / 8]; break;
+    case 1: v = (w + size_t(m3) * m3)[size_t(y / 4) * m2 + x / 4]; break;
+    case 2: v = (w + size_t(m3) * m3 + size_t(m2) * m2)[size_t(y / 2) * m1 + x / 2]; break;
+    default: v = (w + size_t(m3) * m3 + size_t(m2) * m2 + size_t(m1) * m1)[size_t(y) * n + x]; break;
+  }
+  out[i] = v;
+}
+
+// Nonzero count per (layer, row, 128-pixel segment) of an fp32 image.
+__global__ void k_seg_counts_f32(const float* __restrict__ img, int n, int n_layers,
+                                 int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int segs = seg_per_row(n);
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gw >= (long long)n_layers * n * segs) return;
+  const int seg = int(gw % segs);
+  const long long lr = gw / segs;
+  const float* row = img + size_t(lr) * n;
+  int nz = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int x = seg * 128 + 4 * lane + k;
+    nz += (x < n) && row[x] != 0.0f;
+  }
+  for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(kFull, nz, o);
+  if (lane == 0) counts[gw] = nz;
+}
+
 // Mask cell lists (row-major ascending y*m + x), same two-pass scheme.
 __global__ void k_mask_counts(const uint8_t* __restrict__ mask, int m, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
@@ -865,6 +908,21 @@ int launch_expand_residual(const double* h, const double* v, const double* d, in
                            cudaStream_t s) {
   const size_t cnt = size_t(m) * m;
   k_expand_residual<<<unsigned((cnt + 255) / 256), 256, 0, s>>>(h, v, d, m, out);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_stage_delta(const float* w_stage, int n, int n_layers, int stage, float* out,
+                       cudaStream_t s) {
+  const size_t total = size_t(n) * n * n_layers;
+  k_stage_delta<<<unsigned((total + 255) / 256), 256, 0, s>>>(w_stage, n, n_layers, stage, out);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
+int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t s) {
+  const long long warps = (long long)n_layers * n * seg_per_row(n);
+  k_seg_counts_f32<<<unsigned((warps + 7) / 8), 256, 0, s>>>(img, n, n_layers, counts);
   WCGH_CHECK_LAUNCH();
   return 1;
 }

@@ -187,6 +187,10 @@ int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_l
                           int offset, int layer0, wcgh_point* points, cudaStream_t stream);
 // Ordered compaction of nonzero mask bytes into cell indices y*m+x.
 int launch_mask_counts(const uint8_t* mask, int m, int* seg_counts, cudaStream_t stream);
+// Stage s's amplitude contribution image (snapshots of the direct/FFT methods).
+int launch_stage_delta(const float* w_stage, int n, int n_layers, int stage, float* out,
+                       cudaStream_t stream);
+int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t stream);
 int launch_compact_mask(const uint8_t* mask, int m, const int* offsets, uint32_t* cells,
                         cudaStream_t stream);
 
