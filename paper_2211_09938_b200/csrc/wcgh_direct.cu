@@ -54,7 +54,7 @@ __device__ __forceinline__ void layer_span(const long long* lb, int l, long long
   s1 = min(p1, lb[l + 1]);
 }
 
-// NC: phase-series terms (b_2 .. b_{NC+1}); AMP: 0 = MUFU.RSQ, 2/3 = degree of
+// NC: phase-series terms (b_2 .. b_{NC+1}); AMP: 0 = MUFU.RSQ, 1/2/3 = degree of
 // the (1+u)^(-1/2) polynomial.
 template <int P, int NC, int AMP, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
           float am;
           if constexpr (AMP == 3) {
             am = fmaf(fmaf(fmaf(a3, u, a2), u, a1), u, a0);
+          } else if constexpr (AMP == 1) {
+            am = fmaf(a1, u, a0);
           } else if constexpr (AMP == 2) {
             am = fmaf(fmaf(a2, u, a1), u, a0);
           } else {
@@ -263,7 +265,9 @@ void launch_fixed(const LaunchArgs& a) {
 
 template <int P, int NC>
 void launch_fixed_amp(const DirectPlan& plan, const LaunchArgs& a) {
-  if (plan.amp_degree == 2)
+  if (plan.amp_degree == 1)
+    launch_fixed<P, NC, 1>(a);
+  else if (plan.amp_degree == 2)
     launch_fixed<P, NC, 2>(a);
   else if (plan.amp_degree == 3)
     launch_fixed<P, NC, 3>(a);
@@ -324,7 +328,7 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
   const double two_pi = 6.283185307179586476925286766559;
   const double s_max = max_dx * max_dx + max_dy * max_dy;
   int need = 2;
-  bool amp3 = false, amp_rsqrt = false;
+  bool amp2 = false, amp3 = false, amp_rsqrt = false;
   for (int l = 0; l < n_layers; ++l) {
     const double p = layers[l].pitch, z = layers[l].z, K = layers[l].z / layers[l].wavelength;
     const double u = s_max * p * p / (z * z);
@@ -343,15 +347,17 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
     const auto amp_tail = [&](int deg) {
       return std::fabs(binom(-0.5, deg + 1)) * std::pow(u, deg + 1) / (1.0 - u);
     };
-    if (amp_tail(2) > kAmpTol) {
-      if (amp_tail(3) <= kAmpTol)
+    if (amp_tail(1) > kAmpTol) {
+      if (amp_tail(2) <= kAmpTol)
+        amp2 = true;
+      else if (amp_tail(3) <= kAmpTol)
         amp3 = true;
       else
         amp_rsqrt = true;
     }
   }
   plan.n_corr = need <= 2 ? 2 : (need <= 3 ? 3 : (need <= 5 ? 5 : 8));
-  plan.amp_degree = amp_rsqrt ? 0 : (amp3 ? 3 : 2);
+  plan.amp_degree = amp_rsqrt ? 0 : (amp3 ? 3 : (amp2 ? 2 : 1));
   return plan;
 }
 

@@ -86,7 +86,7 @@ struct DirectLayer {
 
 struct DirectPlan {
   int n_corr;      // phase-series terms used (2, 3, 5 or 8)
-  int amp_degree;  // (1+u)^(-1/2): polynomial degree 2 or 3, or 0 = MUFU.RSQ
+  int amp_degree;  // (1+u)^(-1/2): polynomial degree 1, 2 or 3, or 0 = MUFU.RSQ
   double u_max;
 };
 
