@@ -277,6 +277,17 @@ int wcgh_ssim(wcgh_ctx* ctx, const double* a, const double* b, int width, int he
 int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object,
                     const void* saliency, float* out, wcgh_stats* stats);
 
+/* Single-process multi-GPU one-shot: the whole plane
+ * (desc->row0 = 0, rows = plane_size) split into contiguous row bands, one per
+ * listed device (equal splits, remainder to the first; a device may repeat),
+ * each band synthesised on its device by its own host thread and written
+ * straight into its rows of `out` — the band results are bitwise those of a
+ * single-device run. Processes that own one GPU each use the job API per band
+ * and an NCCL all-gather instead (paper_2211_09938_b200/tiles.py). */
+int wcgh_synthesize_multi(int n_devices, const int* devices, const wcgh_desc* desc,
+                          const void* object, const void* saliency, float* out,
+                          wcgh_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,8 @@ _SIGS = [
     ("wcgh_ssim", C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                             C.c_double, C.POINTER(C.c_double)]),
     ("wcgh_synthesize", C.c_int, [_VP, C.POINTER(Desc), _VP, _VP, _VP, C.POINTER(Stats)]),
+    ("wcgh_synthesize_multi", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(Desc), _VP, _VP, _VP,
+                                        C.POINTER(Stats)]),
 ]
 EXPORTED = [s[0] for s in _SIGS]
 

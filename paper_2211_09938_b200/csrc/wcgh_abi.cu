@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "wcgh_internal.cuh"
@@ -1191,6 +1192,70 @@ int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object, co
   if (!rc && stats) rc = wcgh_job_stats(job, stats);
   wcgh_job_destroy(job);
   return rc;
+}
+
+}  // extern "C"
+
+namespace {
+// Row band `rank` of `world` (tiles.band: equal splits, remainder to the
+// first) on `device`, written into its rows of the host plane `out`.
+void synth_band(int rank, int world, int device, const wcgh_desc* desc, const void* object,
+                const void* saliency, float* out, wcgh_stats* st, int* rc_out, std::string* err) {
+  const int n = desc->plane_size;
+  const int base = n / world, rem = n % world;
+  wcgh_desc d = *desc;
+  d.row0 = rank * base + std::min(rank, rem);
+  d.rows = base + (rank < rem ? 1 : 0);
+  wcgh_ctx* ctx = nullptr;
+  int rc = wcgh_create(device, &ctx);
+  if (rc == WCGH_OK) rc = wcgh_synthesize(ctx, &d, object, saliency, out + size_t(2) * d.row0 * n, st);
+  if (rc != WCGH_OK) *err = t_last_error;
+  *rc_out = rc;
+  if (ctx) wcgh_destroy(ctx);
+}
+}  // namespace
+
+extern "C" {
+
+int wcgh_synthesize_multi(int n_devices, const int* devices, const wcgh_desc* desc,
+                          const void* object, const void* saliency, float* out,
+                          wcgh_stats* stats) {
+  return guard(nullptr, [&] {
+    require(n_devices >= 1 && n_devices <= 64, "synthesize_multi: 1..64 devices");
+    require(devices && desc && object && saliency && out, "synthesize_multi: NULL argument");
+    require(desc->row0 == 0 && desc->rows == desc->plane_size,
+            "synthesize_multi: desc must describe the whole plane (row0 = 0, rows = plane_size)");
+    require(n_devices <= desc->plane_size, "synthesize_multi: more devices than plane rows");
+    std::vector<int> rcs(size_t(n_devices), WCGH_OK);
+    std::vector<std::string> errs(static_cast<size_t>(n_devices));
+    std::vector<wcgh_stats> st(static_cast<size_t>(n_devices));
+    std::vector<std::thread> workers;
+    for (int i = 0; i < n_devices; ++i)
+      workers.emplace_back(synth_band, i, n_devices, devices[i], desc, object, saliency, out,
+                           st.data() + i, rcs.data() + i, errs.data() + i);
+    for (auto& w : workers) w.join();
+    for (int i = 0; i < n_devices; ++i) {
+      if (rcs[size_t(i)] == WCGH_EVALIDATION) throw ValidationError(errs[size_t(i)]);
+      if (rcs[size_t(i)] != WCGH_OK)
+        throw RuntimeError(errs[size_t(i)] + " (device " + std::to_string(devices[i]) + ")");
+    }
+    if (stats) {
+      // ops / points come from the (identical, redundant) analysis of every
+      // band; work adds up, times are the slowest band's
+      wcgh_stats agg = st[0];
+      for (int i = 1; i < n_devices; ++i) {
+        const wcgh_stats& t = st[size_t(i)];
+        agg.updates += t.updates;
+        agg.ms_analysis = std::max(agg.ms_analysis, t.ms_analysis);
+        agg.ms_synthesis = std::max(agg.ms_synthesis, t.ms_synthesis);
+        agg.ms_reduce = std::max(agg.ms_reduce, t.ms_reduce);
+        agg.ms_total = std::max(agg.ms_total, t.ms_total);
+        agg.synth_launches += t.synth_launches;
+        agg.total_launches += t.total_launches;
+      }
+      *stats = agg;
+    }
+  });
 }
 
 }  // extern "C"

@@ -37,29 +37,35 @@ _DT = {"u8": L.U8, "f32": L.F32, "f64": L.F64}
 _NP = {"u8": np.uint8, "f32": np.float32, "f64": np.float64}
 
 
+def _make_desc(spec: JobSpec):
+    """wcgh_desc for a spec (and the layer array it points to, kept alive by the caller)."""
+    layers = (L.Layer * len(spec.layers))(*[L.Layer(*t) for t in spec.layers])
+    d = L.Desc()
+    d.object_size = spec.object_size
+    d.plane_size = spec.plane_size
+    d.n_layers = len(spec.layers)
+    d.layers = C.cast(layers, C.POINTER(L.Layer))
+    d.plan = L.Plan(spec.t_ll, spec.t_l, spec.t_full, int(spec.enable_ll),
+                    int(spec.enable_l), int(spec.enable_full))
+    methods = {"direct": L.METHOD_DIRECT, "lut": L.METHOD_LUT, "fft": L.METHOD_FFT}
+    if spec.method not in methods:
+        raise L.ValidationError(f"unknown method {spec.method!r}")
+    d.method = methods[spec.method]
+    d.phase_mode = L.PHASE_FIXED if spec.phase == "fixed" else L.PHASE_FP64
+    d.row0 = spec.row0
+    d.rows = spec.rows if spec.rows is not None else spec.plane_size - spec.row0
+    d.obj_dtype = _DT[spec.obj_dtype]
+    d.obj_scale = spec.obj_scale
+    d.sal_dtype = _DT[spec.sal_dtype]
+    return d, layers
+
+
 class HologramJob:
     def __init__(self, spec: JobSpec, ctx: L.Context | None = None):
         self.ctx = ctx or L.default_context()
         self.spec = spec
         self.rows = spec.rows if spec.rows is not None else spec.plane_size - spec.row0
-        self._layers = (L.Layer * len(spec.layers))(*[L.Layer(*t) for t in spec.layers])
-        d = L.Desc()
-        d.object_size = spec.object_size
-        d.plane_size = spec.plane_size
-        d.n_layers = len(spec.layers)
-        d.layers = C.cast(self._layers, C.POINTER(L.Layer))
-        d.plan = L.Plan(spec.t_ll, spec.t_l, spec.t_full, int(spec.enable_ll),
-                        int(spec.enable_l), int(spec.enable_full))
-        methods = {"direct": L.METHOD_DIRECT, "lut": L.METHOD_LUT, "fft": L.METHOD_FFT}
-        if spec.method not in methods:
-            raise L.ValidationError(f"unknown method {spec.method!r}")
-        d.method = methods[spec.method]
-        d.phase_mode = L.PHASE_FIXED if spec.phase == "fixed" else L.PHASE_FP64
-        d.row0 = spec.row0
-        d.rows = self.rows
-        d.obj_dtype = _DT[spec.obj_dtype]
-        d.obj_scale = spec.obj_scale
-        d.sal_dtype = _DT[spec.sal_dtype]
+        d, self._layers = _make_desc(spec)
         self.desc = d
         h = C.c_void_p()
         L.check(self.ctx.lib.wcgh_job_create(self.ctx.h, C.byref(d), C.byref(h)))
@@ -170,3 +176,20 @@ def spec_for_scene(scene, method: str | None = None, phase: str = "fixed", row0:
 def write_job_cgh1(job: HologramJob, path, stage: int = -1) -> None:
     """The job's last plane (stage < 0) or LUT stage snapshot as a CGH1 file."""
     L.check(job.ctx.lib.wcgh_job_write_cgh1(job.h, str(path).encode(), int(stage)))
+
+
+def synthesize_multi(spec: JobSpec, objects: np.ndarray, masks: np.ndarray, devices) -> tuple:
+    """wcgh_synthesize_multi: the whole plane as row bands over `devices` (one
+    host thread and context each, a device may repeat) -> (plane, stats)."""
+    d, layers = _make_desc(spec)
+    objects = np.ascontiguousarray(objects, _NP[spec.obj_dtype])
+    masks = np.ascontiguousarray(masks, _NP[spec.sal_dtype])
+    n = spec.plane_size
+    out = np.empty((n, n), np.complex64)
+    devs = (C.c_int * len(devices))(*devices)
+    st = L.Stats()
+    L.check(L.load().wcgh_synthesize_multi(len(devices), devs, C.byref(d), L.ptr(objects),
+                                           L.ptr(masks), L.ptr(out), C.byref(st)))
+    del layers
+    return out, {"ops": [int(v) for v in st.ops], "n_points": int(st.n_points),
+                 "updates": float(st.updates), "ms_total": st.ms_total}
