@@ -319,7 +319,7 @@ LutVariant lut_variant() {
 int lut_chunk_target() {
   static const int t = [] {
     const char* e = std::getenv("WCGH_LUT_CHUNKS");
-    return e ? std::max(1, std::atoi(e)) : 24;
+    return e ? std::max(1, std::atoi(e)) : 8;
   }();
   return t;
 }
