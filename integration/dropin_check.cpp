@@ -14,6 +14,7 @@
 #include "wavecgh/haar.hpp"
 #include "wavecgh/saliency.hpp"
 #include "wavecgh/synthesis.hpp"
+#include "wavecgh_gpu.hpp"
 
 extern "C" {
 int ref_haar_analyze(const double* image, int n, int levels, double* out);
@@ -123,6 +124,45 @@ int main() {
     ref_apply_block(wl, pitch, z, n, 2, 1, 2, 0.3, -0.7, pl.data(), &aops);
     EXPECT(rel_l2(plane, pl.data()) <= 1e-5, "apply_block complex weight n=%d", n);
     EXPECT(ac.get(OpLevel::kRefineL) == 1, "apply_block count");
+  }
+  // explicit-method overload and the layered (multi-depth) entry (wavecgh_gpu.hpp)
+  {
+    const int n = 64;
+    const double th[3] = {0.5, 0.7, 0.9};
+    const int en[3] = {1, 1, 1};
+    std::vector<double> planes(std::size_t(8) * n * n), sum(std::size_t(8) * n * n, 0.0);
+    std::vector<std::uint8_t> masks(std::size_t(n) * n * 21 / 16);
+    std::uint64_t ops[5], ops_sum[5] = {0, 0, 0, 0, 0};
+    std::vector<RealImage> objs, sals;
+    std::vector<SceneParams> scenes;
+    for (int l = 0; l < 2; ++l) {
+      const double zl = 0.05 + 0.03 * l;
+      objs.push_back(random_image(n, 300 + l));
+      sals.push_back(random_image(n, 400 + l));
+      scenes.push_back(make_scene(wl, pitch, zl, n));
+      ref_synthesize_progressive(objs[l].data().data(), sals[l].data().data(), n, wl, pitch, zl, th,
+                                 en, 1, 0, 0, planes.data(), masks.data(), ops);
+      for (std::size_t i = 0; i < planes.size(); ++i) sum[i] += planes[i];
+      for (int i = 0; i < 5; ++i) ops_sum[i] += ops[i];
+      if (l == 0) {
+        for (SynthesisMethod m : {SynthesisMethod::kLut, SynthesisMethod::kDirect, SynthesisMethod::kFft}) {
+          const ProgressiveResult r = synthesize_progressive(objs[0], sals[0], scenes[0], RefinementPlan{}, m);
+          for (int st = 0; st < 4; ++st) {
+            const double e = rel_l2(r.stage(st), planes.data() + std::size_t(2) * n * n * st);
+            EXPECT(e <= 1e-4, "method %d stage %d rel L2 %.3e", int(m), st, e);
+          }
+          for (int i = 0; i < 5; ++i) EXPECT(r.ops.get(kAllOpLevels[i]) == ops[i], "method %d ops[%d]", int(m), i);
+        }
+      }
+    }
+    for (SynthesisMethod m : {SynthesisMethod::kLut, SynthesisMethod::kDirect, SynthesisMethod::kFft}) {
+      const ProgressiveResult r = synthesize_progressive_layered(objs, sals, scenes, RefinementPlan{}, m);
+      for (int st = 0; st < 4; ++st) {
+        const double e = rel_l2(r.stage(st), sum.data() + std::size_t(2) * n * n * st);
+        EXPECT(e <= 1e-4, "layered method %d stage %d rel L2 %.3e", int(m), st, e);
+      }
+      for (int i = 0; i < 5; ++i) EXPECT(r.ops.get(kAllOpLevels[i]) == ops_sum[i], "layered ops[%d]", i);
+    }
   }
   // reconstruct of a synthesised hologram (angular_spectrum.cpp:47-61), fp64 on the device
   {

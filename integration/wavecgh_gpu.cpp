@@ -34,6 +34,7 @@
 #include "wavecgh/haar.hpp"
 #include "wavecgh/saliency.hpp"
 #include "wavecgh/synthesis.hpp"
+#include "wavecgh_gpu.hpp"
 #include "wcgh.h"
 
 namespace wavecgh {
@@ -278,6 +279,93 @@ void refine(ComplexField& plane, const RealImage& h, const RealImage& v, const R
   if (mask) *mask = GateMask{2 * m, 2 * m, std::move(on)};
 }
 
+namespace {
+
+int method_code(SynthesisMethod m) {
+  switch (m) {
+    case SynthesisMethod::kLut: return WCGH_METHOD_LUT;
+    case SynthesisMethod::kDirect: return WCGH_METHOD_DIRECT;
+    case SynthesisMethod::kFft: return WCGH_METHOD_FFT;
+  }
+  throw ValidationError("synthesize_progressive: unknown synthesis method");
+}
+
+// One job over L layers (objects/saliencies concatenated layer-major), all
+// four stage snapshots, layer-0 gate masks, operator counts summed.
+ProgressiveResult run_progressive(const std::vector<const RealImage*>& objects,
+                                  const std::vector<const RealImage*>& saliencies,
+                                  const std::vector<SceneParams>& scenes, const RefinementPlan& plan,
+                                  int method) {
+  plan.validate();
+  const int L = int(scenes.size());
+  if (L < 1 || int(objects.size()) != L || int(saliencies.size()) != L)
+    throw ValidationError("synthesize_progressive: one object and saliency per layer");
+  const int n = scenes[0].plane_size();
+  if (n < 8) throw ValidationError("synthesize_progressive: plane_size must be >= 8");
+  std::vector<wcgh_layer> layers;
+  std::vector<double> obj, sal;
+  for (int l = 0; l < L; ++l) {
+    if (scenes[l].plane_size() != n)
+      throw ValidationError("synthesize_progressive: layers must share the plane size");
+    if (objects[l]->width() != n || objects[l]->height() != n)
+      throw ValidationError("synthesize_progressive: object size does not match the scene");
+    if (!saliencies[l]->same_size(*objects[l]))
+      throw ValidationError("synthesize_progressive: saliency size does not match the object");
+    layers.push_back(layer_of(scenes[l]));
+    obj.insert(obj.end(), objects[l]->data().begin(), objects[l]->data().end());
+    sal.insert(sal.end(), saliencies[l]->data().begin(), saliencies[l]->data().end());
+  }
+  wcgh_desc d{};
+  d.object_size = n;
+  d.plane_size = n;
+  d.n_layers = L;
+  d.layers = layers.data();
+  d.plan = wcgh_plan{plan.t_ll, plan.t_l, plan.t_full, int(plan.enable_ll), int(plan.enable_l),
+                     int(plan.enable_full)};
+  d.method = method;
+  d.phase_mode = WCGH_PHASE_FIXED;
+  d.row0 = 0;
+  d.rows = n;
+  d.obj_dtype = WCGH_F64;
+  d.obj_scale = 1.0;
+  d.sal_dtype = WCGH_F64;
+  wcgh_job* job = nullptr;
+  check(wcgh_job_create(gpu(), &d, &job));
+  std::vector<float> stages(std::size_t(8) * n * n);
+  wcgh_stats st{};
+  int rc = wcgh_job_upload(job, obj.data(), sal.data());
+  if (!rc) rc = wcgh_job_run(job);
+  if (!rc) rc = wcgh_job_download_stages(job, stages.data());
+  if (!rc) rc = wcgh_job_stats(job, &st);
+  wcgh_job_destroy(job);
+  check(rc);
+
+  // masks from the analysis entry point (the same K1 gates), layer 0
+  std::vector<uint8_t> masks(std::size_t(n) * n / 16 + std::size_t(n) * n / 4 + std::size_t(n) * n);
+  wcgh_analysis an{};
+  an.masks = masks.data();
+  check(wcgh_analyze(gpu(), objects[0]->data().data(), WCGH_F64, 1.0, saliencies[0]->data().data(),
+                     WCGH_F64, n, &d.plan, 0, 0, &an));
+
+  ProgressiveResult r;
+  const std::size_t n2 = std::size_t(n) * n;
+  auto stage = [&](int s) {
+    return widen(std::vector<float>(stages.begin() + 2 * n2 * s, stages.begin() + 2 * n2 * (s + 1)), n);
+  };
+  r.base_lll = stage(0);
+  r.after_ll = stage(1);
+  r.after_l = stage(2);
+  r.after_full = stage(3);
+  const std::size_t q = n2 / 16, h2 = n2 / 4;
+  r.mask_ll = GateMask{n / 4, n / 4, std::vector<uint8_t>(masks.begin(), masks.begin() + q)};
+  r.mask_l = GateMask{n / 2, n / 2, std::vector<uint8_t>(masks.begin() + q, masks.begin() + q + h2)};
+  r.mask_full = GateMask{n, n, std::vector<uint8_t>(masks.begin() + q + h2, masks.end())};
+  for (int i = 0; i < kOpLevelCount; ++i) r.ops.add(kAllOpLevels[i], st.ops[i]);
+  return r;
+}
+
+}  // namespace
+
 ProgressiveResult synthesize_progressive(const RealImage& object, const RealImage& saliency,
                                          const SceneParams& scene, const RefinementPlan& plan,
                                          const LutSet& luts, int /*workers*/,
@@ -296,55 +384,25 @@ ProgressiveResult synthesize_progressive(const RealImage& object, const RealImag
     throw ValidationError("synthesize_progressive: LUTs built for a different scene");
   if (random_phase_seed)
     throw ValidationError("synthesize_progressive: random initial phase is not supported by the GPU path");
+  // the reference's algorithm (its LutSet argument)
+  return run_progressive({&object}, {&saliency}, {scene}, plan, WCGH_METHOD_LUT);
+}
 
-  const wcgh_layer L = layer_of(scene);
-  wcgh_desc d{};
-  d.object_size = n;
-  d.plane_size = n;
-  d.n_layers = 1;
-  d.layers = &L;
-  d.plan = wcgh_plan{plan.t_ll, plan.t_l, plan.t_full, int(plan.enable_ll), int(plan.enable_l),
-                     int(plan.enable_full)};
-  d.method = WCGH_METHOD_LUT;  // the reference's algorithm (its LutSet argument)
-  d.phase_mode = WCGH_PHASE_FIXED;
-  d.row0 = 0;
-  d.rows = n;
-  d.obj_dtype = WCGH_F64;
-  d.obj_scale = 1.0;
-  d.sal_dtype = WCGH_F64;
-  wcgh_job* job = nullptr;
-  check(wcgh_job_create(gpu(), &d, &job));
-  std::vector<float> stages(std::size_t(8) * n * n);
-  wcgh_stats st{};
-  int rc = wcgh_job_upload(job, object.data().data(), saliency.data().data());
-  if (!rc) rc = wcgh_job_run(job);
-  if (!rc) rc = wcgh_job_download_stages(job, stages.data());
-  if (!rc) rc = wcgh_job_stats(job, &st);
-  wcgh_job_destroy(job);
-  check(rc);
+ProgressiveResult synthesize_progressive(const RealImage& object, const RealImage& saliency,
+                                         const SceneParams& scene, const RefinementPlan& plan,
+                                         SynthesisMethod method, int /*workers*/) {
+  return run_progressive({&object}, {&saliency}, {scene}, plan, method_code(method));
+}
 
-  // masks from the analysis entry point (the same K1 gates)
-  std::vector<uint8_t> masks(std::size_t(n) * n / 16 + std::size_t(n) * n / 4 + std::size_t(n) * n);
-  wcgh_analysis an{};
-  an.masks = masks.data();
-  check(wcgh_analyze(gpu(), object.data().data(), WCGH_F64, 1.0, saliency.data().data(), WCGH_F64,
-                     n, &d.plan, 0, 0, &an));
-
-  ProgressiveResult r;
-  const std::size_t n2 = std::size_t(n) * n;
-  auto stage = [&](int s) {
-    return widen(std::vector<float>(stages.begin() + 2 * n2 * s, stages.begin() + 2 * n2 * (s + 1)), n);
-  };
-  r.base_lll = stage(0);
-  r.after_ll = stage(1);
-  r.after_l = stage(2);
-  r.after_full = stage(3);
-  const std::size_t q = n2 / 16, h2 = n2 / 4;
-  r.mask_ll = GateMask{n / 4, n / 4, std::vector<uint8_t>(masks.begin(), masks.begin() + q)};
-  r.mask_l = GateMask{n / 2, n / 2, std::vector<uint8_t>(masks.begin() + q, masks.begin() + q + h2)};
-  r.mask_full = GateMask{n, n, std::vector<uint8_t>(masks.begin() + q + h2, masks.end())};
-  for (int i = 0; i < kOpLevelCount; ++i) r.ops.add(kAllOpLevels[i], st.ops[i]);
-  return r;
+ProgressiveResult synthesize_progressive_layered(const std::vector<RealImage>& objects,
+                                                 const std::vector<RealImage>& saliencies,
+                                                 const std::vector<SceneParams>& layers,
+                                                 const RefinementPlan& plan,
+                                                 SynthesisMethod method, int /*workers*/) {
+  std::vector<const RealImage*> o, s;
+  for (const auto& x : objects) o.push_back(&x);
+  for (const auto& x : saliencies) s.push_back(&x);
+  return run_progressive(o, s, layers, plan, method_code(method));
 }
 
 ComplexField synthesize_pointwise_oracle(const RealImage& object, const SceneParams& scene,
