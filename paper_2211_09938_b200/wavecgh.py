@@ -471,8 +471,8 @@ def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: Sce
                            plan: RefinementPlan, luts: LutSet, workers: int = 1,
                            random_phase_seed: int | None = None,
                            method: str = "lut") -> ProgressiveResult:
-    """synthesis.cpp:180-253. method "lut" (the reference's algorithm, stage
-    snapshots), "direct" or "fft" (after_full only; earlier stages None)."""
+    """synthesis.cpp:180-253. method "lut" (the reference's algorithm), "direct"
+    or "fft": the same four stage snapshots from each."""
     plan.validate()
     n = scene.plane_size()
     if n < 8:
@@ -494,9 +494,9 @@ def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: Sce
                               "by the GPU path")
     job = _job(n, scene, plan, method)
     try:
-        holo = job(np.ascontiguousarray(obj), np.ascontiguousarray(sal))
+        job(np.ascontiguousarray(obj), np.ascontiguousarray(sal))
         st = job.stats()
-        snaps = job.download_stages() if method == "lut" else None
+        snaps = job.download_stages()
     finally:
         job.close()
     an = stages.analyze(obj, sal, t=(plan.t_ll, plan.t_l, plan.t_full),
@@ -510,10 +510,7 @@ def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: Sce
     r.mask_full = GateMask(n, n, masks[q2 + h2:].reshape(n, n))
     for lev, v in zip(OpLevel, st["ops"]):
         r.ops.add(lev, v)
-    if snaps is not None:
-        r.base_lll, r.after_ll, r.after_l, r.after_full = (s.astype(np.complex128) for s in snaps)
-    else:
-        r.after_full = holo.astype(np.complex128)
+    r.base_lll, r.after_ll, r.after_l, r.after_full = (s.astype(np.complex128) for s in snaps)
     return r
 
 

@@ -403,3 +403,17 @@ def test_acceptance_4_ssim_full_refinement():  # :212-260 (64^2, z = 0.02)
     ro = O.reconstruct(oracle, WL, 8e-6, 0.02)
     rf = O.reconstruct(full.after_full, WL, 8e-6, 0.02)
     assert O.ssim(rf, ro, 8, 0.01, 0.03, ro.max() - ro.min()) >= 0.999
+
+
+@pytest.mark.parametrize("method", ["direct", "fft"])
+def test_progressive_stages_other_methods(ctx, method):
+    """synthesize_progressive with the direct / FFT method returns the same four
+    stage snapshots as the reference (synthesis.hpp:43-54)."""
+    g = golden("ref_random_n32")
+    sc = scene_for(32)
+    luts = W.LutSet.build(sc)
+    r = W.synthesize_progressive(g["object"], g["saliency"], sc, W.RefinementPlan(), luts,
+                                 method=method)
+    for s in range(4):
+        assert O.max_rel_error(r.stage(s), g["planes"][s]) <= MAXREL, s
+    assert [r.ops.get(l) for l in W.ALL_OP_LEVELS] == g["ops"].tolist()
