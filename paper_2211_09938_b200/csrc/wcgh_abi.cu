@@ -135,6 +135,9 @@ void job_validate(const wcgh_desc& d) {
                                      std::to_string(d.plane_size));
   require(d.plane_size <= 16384, "scene: plane_size above 16384 is not supported");
   require(d.object_size <= d.plane_size, "synthesize_progressive: object larger than the plane");
+  // compaction offsets and run lists are int32
+  require(size_t(d.n_layers) * size_t(d.object_size) * size_t(d.object_size) < (size_t(1) << 31),
+          "job: n_layers x object_size^2 must stay below 2^31 samples");
   require((d.plane_size - d.object_size) % 16 == 0,
           "synthesize_progressive: (plane_size - object_size)/2 must be a multiple of 8");
   require(d.row0 >= 0 && d.rows >= 1 && d.row0 + d.rows <= d.plane_size,
