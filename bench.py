@@ -353,7 +353,11 @@ def main():
     ctx = _lib.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter()
     job = HologramJob(spec_for_scene(sc, method=args.method, row0=row0, rows=rows), ctx)
+    torch.cuda.synchronize()
+    precompute_ms = (time.perf_counter() - t_pre) * 1e3  # LUT / fringe-spectrum build + buffers
 
     # resident inputs (device) for the device-timed `value`
     obj_d = torch.from_numpy(sc.objects).cuda()
@@ -491,6 +495,10 @@ def main():
                        "ops": stats["ops"], "parallelism": f"row tiles x{world}",
                        "l2": "flushed between timed steps (256 MiB write, outside the step interval)"},
             "ms_per_hologram": ms_per_step,
+            "precompute_ms": precompute_ms,
+            "precompute_note": ("job creation outside the timed steps: LUT build (K5) for the LUT "
+                                "method, fringe spectra for FFT, buffers (the reference's lut_build "
+                                "is likewise excluded)"),
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t / args.steps},
@@ -504,7 +512,11 @@ def main():
             h_main = job.download()
             for alt in [m for m in ("direct", "lut", "fft") if m != job.spec.method]:
                 try:
+                    torch.cuda.synchronize()
+                    t_pre = time.perf_counter()
                     ajob = HologramJob(spec_for_scene(sc, method=alt), ctx)
+                    torch.cuda.synchronize()
+                    a_pre = (time.perf_counter() - t_pre) * 1e3
                     ajob.upload_dev(obj_d.data_ptr(), sal_d.data_ptr())
                     for _ in range(args.warmup):
                         ajob.run()
@@ -528,6 +540,7 @@ def main():
                                     "lut": "the reference's block-LUT superposition (K4)",
                                     "fft": "correlation with the point fringe via cuFFT, O(Nh^2 log Nh)"}[alt]),
                         "algorithmic_updates": ast["updates"],
+                        "precompute_ms": a_pre,
                         "rel_l2_vs_main": float(np.linalg.norm(h_alt - h_main) / np.linalg.norm(h_main)),
                     })
                     ajob.close()
