@@ -272,6 +272,22 @@ int wcgh_job_reconstruct(wcgh_job* job, const wcgh_layer* scene, int intensity, 
 int wcgh_ssim(wcgh_ctx* ctx, const double* a, const double* b, int width, int height, int window,
               double k1, double k2, double dynamic_range, double* score);
 
+/* ---- CGHL LUT cache files (fringe_lut.cpp:95-166, lut_cache_store/load) ---
+ * "CGHL", u16 version = 1, u16 block size, u32 N, f64 wavelength, f64 pitch,
+ * f64 z (native little endian, 36 bytes), then (2N-1)^2 interleaved f32
+ * (re, im) — the layout wcgh_build_block_lut returns and the jobs keep on
+ * the device. File errors return WCGH_ERUNTIME (IoError class). */
+int wcgh_write_cghl(const char* path, const float* lut, int n, int block, const wcgh_layer* scene);
+/* Header into *n_out / *block_out / *scene_out (any may be NULL); payload into
+ * `lut` if non-NULL and capacity >= (2N-1)^2 complex64. Scene / block checks
+ * against an expected LUT (StaleCacheError) are the caller's. */
+int wcgh_read_cghl(const char* path, float* lut, int64_t capacity, int* n_out, int* block_out,
+                   wcgh_layer* scene_out);
+/* LUT-method job: replace the block-`block` LUT of `layer` (built at job
+ * creation) with caller data, (2N-1)^2 complex64 — e.g. a reference CGHL
+ * cache, so the job superposes exactly the reference's LUT samples. */
+int wcgh_job_load_lut(wcgh_job* job, int layer, int block, const float* lut);
+
 /* One-shot: job create + upload + run + download + destroy. The entry the
  * C++ synthesize_progressive mirror calls (synthesis.hpp:88-91). */
 int wcgh_synthesize(wcgh_ctx* ctx, const wcgh_desc* desc, const void* object,

@@ -364,6 +364,11 @@ def ref_random_image(w, h, seed):
     return out
 
 
+def ref_lut_cache_store(path, wl, pitch, z, n, block):
+    _ref_check(ref().ref_lut_cache_store(str(path).encode(), C.c_double(wl), C.c_double(pitch),
+                                         C.c_double(z), C.c_int(n), C.c_int(block)))
+
+
 def ref_reconstruct(holo, wl, pitch, z, intensity=False):
     holo = np.ascontiguousarray(holo, np.complex128)
     n = holo.shape[0]

@@ -136,6 +136,12 @@ int ref_build_block_lut(double wl, double pitch, double z, int n, int block, int
   });
 }
 
+// lut_cache_store (fringe_lut.cpp:95-115): the reference's CGHL file of a
+// freshly built LUT.
+int ref_lut_cache_store(const char* path, double wl, double pitch, double z, int n, int block) {
+  return guard([&] { lut_cache_store(build_block_lut(make_scene(wl, pitch, z, n), block, 0), path); });
+}
+
 // apply_block (synthesis.cpp:149-160) on a caller plane with a freshly built LUT.
 int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx, int cy,
                     double w_re, double w_im, double* plane, std::uint64_t* ops) {

@@ -100,6 +100,10 @@ _SIGS = [
     ("wcgh_job_reconstruct", C.c_int, [_VP, C.POINTER(Layer), C.c_int, _VP]),
     ("wcgh_ssim", C.c_int, [_VP, _VP, _VP, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                             C.c_double, C.POINTER(C.c_double)]),
+    ("wcgh_write_cghl", C.c_int, [C.c_char_p, _VP, C.c_int, C.c_int, C.POINTER(Layer)]),
+    ("wcgh_read_cghl", C.c_int, [C.c_char_p, _VP, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                 C.POINTER(Layer)]),
+    ("wcgh_job_load_lut", C.c_int, [_VP, C.c_int, C.c_int, _VP]),
     ("wcgh_synthesize", C.c_int, [_VP, C.POINTER(Desc), _VP, _VP, _VP, C.POINTER(Stats)]),
     ("wcgh_synthesize_multi", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(Desc), _VP, _VP, _VP,
                                         C.POINTER(Stats)]),

@@ -1011,6 +1011,91 @@ int wcgh_read_cgh1(const char* path, float* plane, int64_t capacity, int* n_out,
   });
 }
 
+// ---- CGHL LUT cache files (fringe_lut.cpp:95-166): 36-byte header + f32 ----
+
+int wcgh_write_cghl(const char* path, const float* lut, int n, int block, const wcgh_layer* scene) {
+  return guard(nullptr, [&] {
+    require(path && lut && scene, "lut cache: NULL argument");
+    validate_layer(*scene);
+    require(is_pow2(n), "scene: plane_size must be a power of two, got " + std::to_string(n));
+    require(block == 1 || block == 2 || block == 4 || block == 8,
+            "build_block_lut: unsupported block size " + std::to_string(block));
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw RuntimeError(std::string("lut cache: cannot open ") + path + " for writing");
+    const char magic[4] = {'C', 'G', 'H', 'L'};
+    const uint16_t version = 1, b = uint16_t(block);
+    const uint32_t un = uint32_t(n);
+    bool ok = std::fwrite(magic, 1, 4, f) == 4 && std::fwrite(&version, 2, 1, f) == 1 &&
+              std::fwrite(&b, 2, 1, f) == 1 && std::fwrite(&un, 4, 1, f) == 1 &&
+              std::fwrite(&scene->wavelength, 8, 1, f) == 1 &&
+              std::fwrite(&scene->pitch, 8, 1, f) == 1 && std::fwrite(&scene->z, 8, 1, f) == 1;
+    const size_t span = size_t(2 * n - 1);
+    const size_t count = span * span * 2;
+    ok = ok && std::fwrite(lut, sizeof(float), count, f) == count;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw RuntimeError(std::string("lut cache: write failed for ") + path);
+  });
+}
+
+int wcgh_read_cghl(const char* path, float* lut, int64_t capacity, int* n_out, int* block_out,
+                   wcgh_layer* scene_out) {
+  return guard(nullptr, [&] {
+    require(path != nullptr, "lut cache: NULL path");
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw RuntimeError(std::string("lut cache: cannot open ") + path);
+    struct Closer {
+      std::FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "CGHL", 4) != 0)
+      throw RuntimeError(std::string("lut cache: bad magic in ") + path);
+    uint16_t version = 0, block = 0;
+    uint32_t un = 0;
+    wcgh_layer sc{};
+    if (std::fread(&version, 2, 1, f) != 1 || std::fread(&block, 2, 1, f) != 1 ||
+        std::fread(&un, 4, 1, f) != 1 || std::fread(&sc.wavelength, 8, 1, f) != 1 ||
+        std::fread(&sc.pitch, 8, 1, f) != 1 || std::fread(&sc.z, 8, 1, f) != 1)
+      throw RuntimeError("lut cache: truncated header");
+    if (version != 1) throw RuntimeError("lut cache: unsupported version " + std::to_string(version));
+    require(un > 0 && un <= 65536 && is_pow2(int(un)),
+            "scene: plane_size must be a power of two, got " + std::to_string(un));
+    if (n_out) *n_out = int(un);
+    if (block_out) *block_out = int(block);
+    if (scene_out) *scene_out = sc;
+    if (lut) {
+      const size_t span = size_t(2 * un - 1);
+      const size_t count = span * span;
+      require(capacity >= int64_t(count), "lut cache: output buffer too small");
+      if (std::fread(lut, sizeof(float) * 2, count, f) != count)
+        throw RuntimeError("lut cache: truncated payload");
+      for (size_t i = 0; i < 2 * count; ++i)
+        if (!std::isfinite(lut[i]))
+          throw ValidationError(std::string("lut cache ") + path + ": non-finite sample");
+    }
+  });
+}
+
+int wcgh_job_load_lut(wcgh_job* job, int layer, int block, const float* lut) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && lut, "job_load_lut: NULL argument");
+    require(job->desc.method == WCGH_METHOD_LUT, "job_load_lut: the job does not use the LUT method");
+    require(layer >= 0 && layer < job->desc.n_layers, "job_load_lut: layer out of range");
+    int st = -1;
+    const int blocks[4] = {8, 4, 2, 1};
+    for (int k = 0; k < 4; ++k)
+      if (blocks[k] == block) st = k;
+    require(st >= 0, "build_block_lut: unsupported block size " + std::to_string(block));
+    for (int i = 0; i < 2 * (2 * job->desc.plane_size - 1) * (2 * job->desc.plane_size - 1); ++i)
+      if (!std::isfinite(lut[i])) throw ValidationError("lut: non-finite sample");
+    use_device(job->ctx);
+    const size_t span = size_t(2 * job->desc.plane_size - 1);
+    WCGH_CUDA(cudaMemcpyAsync(job->lut_base[size_t(layer) * 4 + st], lut, sizeof(float2) * span * span,
+                              cudaMemcpyHostToDevice, job->ctx->stream));
+    sync(job->ctx->stream);
+  });
+}
+
 int wcgh_job_write_cgh1(wcgh_job* job, const char* path, int stage) {
   return guard(job ? job->ctx : nullptr, [&] {
     require(job && path, "job_write_cgh1: NULL argument");

@@ -146,6 +146,11 @@ class HologramJob:
                                                   L.ptr(out)))
         return out
 
+    def load_lut(self, layer: int, block: int, lut: np.ndarray) -> None:
+        """LUT method: use caller LUT samples (e.g. a CGHL cache) for (layer, block)."""
+        lut = np.ascontiguousarray(lut, np.complex64)
+        L.check(self.ctx.lib.wcgh_job_load_lut(self.h, int(layer), int(block), L.ptr(lut)))
+
     def plane_dev_ptr(self) -> int:
         return int(self.ctx.lib.wcgh_job_plane_dev(self.h) or 0)
 

@@ -247,3 +247,25 @@ def ssim(a: np.ndarray, b: np.ndarray, window: int = 8, k1: float = 0.01, k2: fl
     L.check(c.lib.wcgh_ssim(c.h, L.ptr(a), L.ptr(b), w, h, int(window), float(k1), float(k2),
                             float(dynamic_range), C.byref(out)))
     return float(out.value)
+
+
+def write_cghl(path, lut: np.ndarray, n: int, block: int, layer) -> None:
+    """lut_cache_store (fringe_lut.cpp:95-115): CGHL header + f32 (re, im) payload."""
+    lut = np.ascontiguousarray(lut, np.complex64)
+    if lut.shape != (2 * n - 1, 2 * n - 1):
+        raise L.ValidationError("lut cache: support size does not match the plane size")
+    lay = L.Layer(*layer)
+    L.check(L.load().wcgh_write_cghl(str(path).encode(), L.ptr(lut), n, int(block), C.byref(lay)))
+
+
+def read_cghl(path):
+    """CGHL file -> (lut complex64 (2N-1)^2, N, block, (wavelength, pitch, z))."""
+    lib = L.load()
+    n, b = C.c_int(0), C.c_int(0)
+    lay = L.Layer()
+    L.check(lib.wcgh_read_cghl(str(path).encode(), None, 0, C.byref(n), C.byref(b), C.byref(lay)))
+    span = 2 * n.value - 1
+    lut = np.empty((span, span), np.complex64)
+    L.check(lib.wcgh_read_cghl(str(path).encode(), L.ptr(lut), lut.size, C.byref(n), C.byref(b),
+                               C.byref(lay)))
+    return lut, n.value, b.value, (lay.wavelength, lay.pitch, lay.z)

@@ -7,7 +7,8 @@ free functions and types (paths under /root/reference/proj):
   haar.hpp:14-51         DetailBands, HaarPyramid, haar_analyze, haar_synthesize,
                          expand_residual, upsample_replicate
   saliency.hpp:11-30     SaliencyPyramid, quantize_saliency, uniform_saliency
-  fringe_lut.hpp:15-62   point_fringe, FringeLut, build_block_lut, LutSet
+  fringe_lut.hpp:15-62   point_fringe, FringeLut, build_block_lut, LutSet,
+                         lut_cache_store, lut_cache_load (CGHL files)
   synthesis.hpp:18-104   RefinementPlan, GateMask, ProgressiveResult, GridCell,
                          apply_block, synthesize_base, refine,
                          synthesize_progressive, synthesize_pointwise_oracle
@@ -298,6 +299,23 @@ def build_block_lut(scene: SceneParams, block_size: int, workers: int = 1) -> Fr
         raise ValidationError("build_block_lut: block size exceeds plane size")
     sup = stages.build_block_lut(scene.layer(), scene.plane_size(), block_size)
     return FringeLut(scene, block_size, sup)
+
+
+def lut_cache_store(lut: FringeLut, path) -> None:
+    """fringe_lut.cpp:95-115: CGHL header + f32 (re, im) payload."""
+    stages.write_cghl(path, lut.support(), lut.scene().plane_size(), lut.block_size(),
+                      lut.scene().layer())
+
+
+def lut_cache_load(path, expected_scene: SceneParams, expected_block_size: int) -> FringeLut:
+    """fringe_lut.cpp:117-166: IoError for unreadable / malformed files,
+    StaleCacheError when the block size or scene does not match."""
+    support, n, block, layer = stages.read_cghl(path)
+    if block != expected_block_size:
+        raise StaleCacheError(f"lut cache: block size {block} != expected {expected_block_size}")
+    if n != expected_scene.plane_size() or tuple(layer) != tuple(expected_scene.layer()):
+        raise StaleCacheError(f"lut cache: scene parameters in {path} do not match the requested scene")
+    return FringeLut(expected_scene, expected_block_size, support)
 
 
 class LutSet:

@@ -132,6 +132,15 @@ def main():
     rec["ssim_value"] = np.array(sv)
     save("ref_recon_ssim", **rec)
 
+    # 9. A CGHL LUT cache file written by the reference (lut_cache_store,
+    #    fringe_lut.cpp:95-115): 16^2 plane, block 2, z = 0.1.
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        path = Path(td) / "lut.cghl"
+        O.ref_lut_cache_store(path, WL, 8e-6, 0.1, 16, 2)
+        save("ref_cghl_n16_b2", cghl_bytes=np.frombuffer(path.read_bytes(), np.uint8),
+             lut=O.ref_build_block_lut(WL, 8e-6, 0.1, 16, 2))
+
 
 if __name__ == "__main__":
     main()

@@ -43,3 +43,39 @@ def test_cgh1_errors(tmp_path):
         stages.read_cgh1(tmp_path / "nan.cgh")
     with pytest.raises(_lib.ValidationError):
         stages.write_cgh1(tmp_path / "x.cgh", plane, (0.0, 8e-6, 0.2))
+
+
+# ---- CGHL LUT cache files (fringe_lut.cpp:95-166) ------------------------------
+
+def test_cghl_bytes_identical_to_reference_writer(tmp_path):
+    """Our writer, given the reference's LUT samples, produces the reference's
+    own CGHL file byte for byte (header + f32 payload, lut_cache_store)."""
+    from conftest import golden
+    g = golden("ref_cghl_n16_b2")
+    p = tmp_path / "lut.cghl"
+    stages.write_cghl(p, g["lut"].astype(np.complex64), 16, 2, (532e-9, 8e-6, 0.1))
+    assert p.read_bytes() == g["cghl_bytes"].tobytes()
+    # and reads the reference's file back (lut_cache_load's header fields)
+    ref_file = tmp_path / "ref.cghl"
+    ref_file.write_bytes(g["cghl_bytes"].tobytes())
+    lut, n, block, scene = stages.read_cghl(ref_file)
+    assert (n, block, scene) == (16, 2, (532e-9, 8e-6, 0.1))
+    assert np.array_equal(lut, g["lut"].astype(np.complex64))
+    magic, version, b, size = struct.unpack("<4sHHI", g["cghl_bytes"].tobytes()[:12])
+    assert (magic, version, b, size) == (b"CGHL", 1, 2, 16)
+
+
+def test_cghl_errors(tmp_path):
+    from conftest import golden
+    raw = golden("ref_cghl_n16_b2")["cghl_bytes"].tobytes()
+    cases = {"magic": b"XGHL" + raw[4:], "version": raw[:4] + b"\x02\x00" + raw[6:],
+             "truncated": raw[:-8], "header": raw[:20]}
+    for name, data in cases.items():
+        p = tmp_path / f"{name}.cghl"
+        p.write_bytes(data)
+        with pytest.raises(_lib.IoError):
+            stages.read_cghl(p)
+    with pytest.raises(_lib.IoError):
+        stages.read_cghl(tmp_path / "missing.cghl")
+    with pytest.raises(_lib.ValidationError):
+        stages.write_cghl(tmp_path / "x.cghl", np.zeros((5, 5), np.complex64), 16, 2, (532e-9, 8e-6, 0.1))

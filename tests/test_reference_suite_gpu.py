@@ -417,3 +417,37 @@ def test_progressive_stages_other_methods(ctx, method):
     for s in range(4):
         assert O.max_rel_error(r.stage(s), g["planes"][s]) <= MAXREL, s
     assert [r.ops.get(l) for l in W.ALL_OP_LEVELS] == g["ops"].tolist()
+
+
+# ---- test_fringe_lut.cpp: LUT cache (CGHL) ---------------------------------
+
+def test_lut_cache_round_trip(ctx, tmp_path):  # :135-156
+    sc = scene_for(16)
+    lut = W.build_block_lut(sc, 2)
+    p = tmp_path / "lut_b2.cghl"
+    W.lut_cache_store(lut, p)
+    loaded = W.lut_cache_load(p, sc, 2)
+    assert loaded.block_size() == 2 and loaded.scene() == sc
+    assert np.array_equal(loaded.support(), lut.support().astype(np.complex64))
+    copy = tmp_path / "copy.cghl"
+    W.lut_cache_store(loaded, copy)
+    assert p.read_bytes() == copy.read_bytes()
+
+
+def test_lut_cache_validation(ctx, tmp_path):  # :158-189
+    sc = scene_for(16)
+    p = tmp_path / "lut_b1.cghl"
+    W.lut_cache_store(W.build_block_lut(sc, 1), p)
+    with pytest.raises(W.StaleCacheError):
+        W.lut_cache_load(p, W.make_scene(633e-9, 8e-6, 0.1, 16), 1)
+    with pytest.raises(W.StaleCacheError):
+        W.lut_cache_load(p, sc, 2)
+    raw = p.read_bytes()
+    (tmp_path / "truncated.cghl").write_bytes(raw[: len(raw) // 2])
+    with pytest.raises(W.IoError):
+        W.lut_cache_load(tmp_path / "truncated.cghl", sc, 1)
+    (tmp_path / "bad.cghl").write_bytes(b"XXXXnotalut")
+    with pytest.raises(W.IoError):
+        W.lut_cache_load(tmp_path / "bad.cghl", sc, 1)
+    with pytest.raises(W.IoError):
+        W.lut_cache_load(tmp_path / "absent.cghl", sc, 1)
