@@ -299,14 +299,14 @@ constexpr int kMaxChunkSteps = 4096;
 constexpr size_t kPartialBytes = 2ull << 30;
 
 // Register-window shape: R rows x PX columns per thread, D rows of prefetch,
-// W warps per CTA. Default 8 x 2 x 4 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
+// W warps per CTA. Default 8 x 2 x 2 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
 // another compiled shape (tuning only; results equal up to fp32 rounding).
 struct LutVariant {
   int R, PX, D, W;
 };
 LutVariant lut_variant() {
   static const LutVariant v = [] {
-    LutVariant d{8, 2, 4, 4};
+    LutVariant d{8, 2, 2, 4};
     if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
       int r = 0, px = 0, dd = 0, w = 4;
       const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
@@ -344,12 +344,12 @@ void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageC
                                        chunk_steps, out, stride, s);                        \
     return;                                                                                 \
   }
-  WCGH_V(8, 4, 2, 4)
   WCGH_V(8, 2, 2, 4)
+  WCGH_V(8, 2, 1, 4)
+  WCGH_V(8, 2, 3, 4)
   WCGH_V(8, 2, 4, 4)
-  WCGH_V(8, 2, 6, 4)
-  WCGH_V(8, 2, 4, 8)
-  WCGH_V(16, 2, 4, 4)
+  WCGH_V(8, 2, 2, 8)
+  WCGH_V(8, 4, 2, 4)
   WCGH_V(16, 2, 2, 4)
 #undef WCGH_V
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
