@@ -694,14 +694,11 @@ __device__ __forceinline__ void cell_u8(const uint2 (&ov)[8], const uint2 (&sv)[
 
   // operator counts (synthesis.cpp:68, 77-88): every LLL cell, gated cells
   int n_ll = valid ? int(G2[0][0]) + int(G2[0][1]) + int(G2[1][0]) + int(G2[1][1]) : 0;
-  int n_b = valid ? 1 : 0;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    n_b += __shfl_xor_sync(kFull, n_b, o);
-    n_ll += __shfl_xor_sync(kFull, n_ll, o);
-    n_l += __shfl_xor_sync(kFull, n_l, o);
-    n_f += __shfl_xor_sync(kFull, n_f, o);
-  }
+  // warp sums by the hardware reduction (REDUX), one instruction each
+  const int n_b = __reduce_add_sync(kFull, valid ? 1 : 0);
+  n_ll = __reduce_add_sync(kFull, n_ll);
+  n_l = __reduce_add_sync(kFull, n_l);
+  n_f = __reduce_add_sync(kFull, n_f);
   if (lane == 0 && n_b) {
     unsigned long long* ops = out.ops + layer * WCGH_OP_LEVELS;
     atomicAdd(ops + WCGH_OP_BASE_LLL, (unsigned long long)n_b);
@@ -712,11 +709,9 @@ __device__ __forceinline__ void cell_u8(const uint2 (&ov)[8], const uint2 (&sv)[
 
   // nonzero counts per (row, 128-pixel segment) = 16 consecutive cells
   if (out.seg_counts) {
-#pragma unroll
-    for (int o = 8; o; o >>= 1) {
-      cnt_lo += __shfl_xor_sync(kFull, cnt_lo, o);
-      cnt_hi += __shfl_xor_sync(kFull, cnt_hi, o);
-    }
+    const unsigned half = lane < 16 ? 0x0000ffffu : 0xffff0000u;  // one segment per half-warp
+    cnt_lo = __reduce_add_sync(half, cnt_lo);
+    cnt_hi = __reduce_add_sync(half, cnt_hi);
     if ((lane & 15) == 0 && valid) {
       const int segs = seg_per_row(n);
       const int seg = X0 / 128;
