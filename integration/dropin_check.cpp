@@ -26,6 +26,7 @@ int ref_synthesize_progressive(const double* object, const double* saliency, int
 int ref_synthesize_pointwise_oracle(const double* object, int n, double wl, double pitch, double z,
                                     int workers, double* out, std::uint64_t* ops);
 int ref_random_image(int w, int h, std::uint64_t seed, double* out);
+int ref_build_block_lut(double wl, double pitch, double z, int n, int block, int workers, double* out);
 int ref_reconstruct(const double* holo, int n, double wl, double pitch, double z, int intensity,
                     double* out);
 int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx, int cy,
@@ -124,6 +125,40 @@ int main() {
     ref_apply_block(wl, pitch, z, n, 2, 1, 2, 0.3, -0.7, pl.data(), &aops);
     EXPECT(rel_l2(plane, pl.data()) <= 1e-5, "apply_block complex weight n=%d", n);
     EXPECT(ac.get(OpLevel::kRefineL) == 1, "apply_block count");
+  }
+  // fringe_lut.cpp on the device: build_block_lut vs the reference's fp64 LUT
+  // (complex64 precision), CGHL round trip through the reference's format
+  {
+    const SceneParams scene = make_scene(wl, pitch, z, 32);
+    for (int b : {1, 2, 4, 8}) {
+      const FringeLut g = build_block_lut(scene, b);
+      std::vector<double> ref(std::size_t(2) * 63 * 63);
+      ref_build_block_lut(wl, pitch, z, 32, b, 1, ref.data());
+      double md = 0, mr = 0;
+      for (std::size_t i = 0; i < g.support().size(); ++i) {
+        const std::complex<double> r(ref[2 * i], ref[2 * i + 1]);
+        md = std::max(md, std::abs(g.support().data()[i] - r));
+        mr = std::max(mr, std::abs(r));
+      }
+      EXPECT(md <= 2e-7 * mr, "build_block_lut b=%d max rel %.3e", b, md / mr);
+      EXPECT(std::abs(g.at_offset(0, 0) - g.support().at(31, 31)) == 0.0, "at_offset");
+    }
+    const FringeLut l2 = build_block_lut(scene, 2);
+    const std::string path = "/tmp/dropin_lut_b2.cghl";
+    lut_cache_store(l2, path);
+    const FringeLut back = lut_cache_load(path, scene, 2);
+    bool same = true;
+    for (std::size_t i = 0; i < l2.support().size(); ++i) same = same && back.support().data()[i] == l2.support().data()[i];
+    EXPECT(same, "lut cache round trip");
+    bool stale = false;
+    try {
+      lut_cache_load(path, scene, 4);
+    } catch (const StaleCacheError&) {
+      stale = true;
+    }
+    EXPECT(stale, "lut cache block mismatch must throw StaleCacheError");
+    const LutSet set = LutSet::build(scene);
+    EXPECT(set.has(1) && set.has(8) && set.of(4).block_size() == 4, "LutSet");
   }
   // explicit-method overload and the layered (multi-depth) entry (wavecgh_gpu.hpp)
   {

@@ -1,10 +1,11 @@
 // Drop-in GPU implementation of the reference's hot-path C++ API.
 //
 // Compile this file INSTEAD OF the reference's core/src/synthesis.cpp,
-// core/src/haar.cpp, core/src/saliency.cpp and core/src/angular_spectrum.cpp
-// (keep the reference headers and its other sources) and link libwcgh.so:
-// every entry point keeps its signature (synthesis.hpp:70-104,
-// haar.hpp:36-51, saliency.hpp:25-30, angular_spectrum.hpp:17-27) and its
+// core/src/haar.cpp, core/src/saliency.cpp, core/src/angular_spectrum.cpp and
+// core/src/fringe_lut.cpp (keep the reference headers and its other sources)
+// and link libwcgh.so: every entry point keeps its signature
+// (synthesis.hpp:70-104, haar.hpp:36-51, saliency.hpp:25-30,
+// angular_spectrum.hpp:17-27, fringe_lut.hpp:15-62) and its
 // ValidationError behaviour, and runs on the sm_100a kernels through the C ABI
 // (include/wcgh.h). There is no CPU fallback: without a CUDA device the calls
 // throw IoError (the reference's exit-code-2 class).
@@ -15,6 +16,9 @@
 //  * `workers` is accepted and ignored (results are launch-invariant);
 //  * random_phase_seed is rejected (complex amplitudes are out of scope,
 //    DESIGN.md §7); random_phase_field itself stays a host RNG function;
+//  * build_block_lut runs on the device (K5: fp64 sums, complex64 store — the
+//    CGHL payload precision) and is widened to the FringeLut's
+//    complex<double>; lut_cache_store/load go through the ABI's CGHL I/O;
 //  * build_kernel / propagate / reconstruct run in fp64 like the reference
 //    (cuFFT Z2Z); propagate evaluates the transfer function of
 //    (kernel.scene, kernel.z_signed) on the device, i.e. kernel.transfer as
@@ -31,6 +35,7 @@
 
 #include "wavecgh/angular_spectrum.hpp"
 #include "wavecgh/errors.hpp"
+#include "wavecgh/fringe_lut.hpp"
 #include "wavecgh/haar.hpp"
 #include "wavecgh/saliency.hpp"
 #include "wavecgh/synthesis.hpp"
@@ -475,6 +480,115 @@ RealImage reconstruct(const ComplexField& hologram, const SceneParams& scene, bo
   check(wcgh_reconstruct(gpu(), hologram.data().data(), WCGH_F64, n, &L, intensity ? 1 : 0,
                          img.data()));
   return RealImage(n, n, std::move(img));
+}
+
+// ---- fringe_lut.cpp:27-196 ----------------------------------------------------
+
+namespace {
+bool supported_block(int b) {
+  return std::find(kLutBlockSizes.begin(), kLutBlockSizes.end(), b) != kLutBlockSizes.end();
+}
+}  // namespace
+
+std::complex<double> point_fringe(const SceneParams& scene, int dx, int dy) {
+  const double px = dx * scene.pitch();
+  const double py = dy * scene.pitch();
+  const double r = std::sqrt(px * px + py * py + scene.z() * scene.z());
+  return std::polar(1.0 / r, scene.wave_number() * r);
+}
+
+FringeLut::FringeLut(SceneParams scene, int block_size, ComplexField support)
+    : scene_(scene), block_size_(block_size), support_(std::move(support)) {
+  if (!supported_block(block_size_))
+    throw ValidationError("FringeLut: unsupported block size " + std::to_string(block_size_));
+  const int expected = 2 * scene_.plane_size() - 1;
+  if (support_.width() != expected || support_.height() != expected)
+    throw ValidationError("FringeLut: support must be (2N-1) x (2N-1)");
+}
+
+std::complex<double> FringeLut::at_offset(int dx, int dy) const {
+  const int n = scene_.plane_size();
+  if (dx <= -n || dx >= n || dy <= -n || dy >= n)
+    throw ValidationError("FringeLut: offset outside support");
+  return support_.at(dx + n - 1, dy + n - 1);
+}
+
+FringeLut build_block_lut(const SceneParams& scene, int block_size, int /*workers*/) {
+  if (!supported_block(block_size))
+    throw ValidationError("build_block_lut: unsupported block size " + std::to_string(block_size));
+  const int n = scene.plane_size();
+  if (block_size > n) throw ValidationError("build_block_lut: block size exceeds plane size");
+  const int span = 2 * n - 1;
+  const wcgh_layer L = layer_of(scene);
+  std::vector<float> c(std::size_t(2) * span * span);
+  check(wcgh_build_block_lut(gpu(), &L, n, block_size, c.data()));
+  ComplexField support(span, span);
+  for (std::size_t i = 0; i < support.size(); ++i)
+    support.data()[i] = {double(c[2 * i]), double(c[2 * i + 1])};
+  return FringeLut(scene, block_size, std::move(support));
+}
+
+void lut_cache_store(const FringeLut& lut, const std::filesystem::path& path) {
+  const auto& samples = lut.support().data();
+  std::vector<float> payload(samples.size() * 2);
+  for (std::size_t i = 0; i < samples.size(); ++i) {
+    payload[2 * i] = float(samples[i].real());
+    payload[2 * i + 1] = float(samples[i].imag());
+  }
+  const wcgh_layer L = layer_of(lut.scene());
+  check(wcgh_write_cghl(path.string().c_str(), payload.data(), lut.scene().plane_size(),
+                        lut.block_size(), &L));
+}
+
+FringeLut lut_cache_load(const std::filesystem::path& path, const SceneParams& expected_scene,
+                         int expected_block_size) {
+  int n = 0, block = 0;
+  wcgh_layer sc{};
+  check(wcgh_read_cghl(path.string().c_str(), nullptr, 0, &n, &block, &sc));
+  if (block != expected_block_size)
+    throw StaleCacheError("lut cache: block size " + std::to_string(block) + " != expected " +
+                          std::to_string(expected_block_size));
+  if (n != expected_scene.plane_size() || sc.wavelength != expected_scene.wavelength() ||
+      sc.pitch != expected_scene.pitch() || sc.z != expected_scene.z())
+    throw StaleCacheError("lut cache: scene parameters in " + path.string() +
+                          " do not match the requested scene");
+  const std::size_t span = std::size_t(2 * n - 1);
+  std::vector<float> payload(2 * span * span);
+  check(wcgh_read_cghl(path.string().c_str(), payload.data(), int64_t(span * span), &n, &block, &sc));
+  ComplexField support(static_cast<int>(span), static_cast<int>(span));
+  for (std::size_t i = 0; i < support.size(); ++i)
+    support.data()[i] = {double(payload[2 * i]), double(payload[2 * i + 1])};
+  return FringeLut(expected_scene, expected_block_size, std::move(support));
+}
+
+LutSet LutSet::build(const SceneParams& scene, int workers) {
+  LutSet set;
+  for (int b : kLutBlockSizes) set.put(build_block_lut(scene, b, workers));
+  return set;
+}
+
+void LutSet::put(FringeLut lut) {
+  if (!luts_.empty() && !(luts_.front().scene() == lut.scene()))
+    throw ValidationError("LutSet: mixed scene parameters");
+  for (auto& existing : luts_) {
+    if (existing.block_size() == lut.block_size()) {
+      existing = std::move(lut);
+      return;
+    }
+  }
+  luts_.push_back(std::move(lut));
+}
+
+bool LutSet::has(int block_size) const {
+  for (const auto& lut : luts_)
+    if (lut.block_size() == block_size) return true;
+  return false;
+}
+
+const FringeLut& LutSet::of(int block_size) const {
+  for (const auto& lut : luts_)
+    if (lut.block_size() == block_size) return lut;
+  throw ValidationError("LutSet: no LUT for block size " + std::to_string(block_size));
 }
 
 }  // namespace wavecgh

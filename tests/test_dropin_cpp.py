@@ -1,5 +1,5 @@
 """The reference's own C++ API backed by the GPU (integration/wavecgh_gpu.cpp
-replacing synthesis.cpp, haar.cpp, saliency.cpp, angular_spectrum.cpp) against
+replacing synthesis.cpp, haar.cpp, saliency.cpp, angular_spectrum.cpp, fringe_lut.cpp) against
 the unmodified CPU reference. The binary is built here by integration/Makefile (it needs the
 reference headers) and travels to the GPU box prebuilt."""
 import subprocess
