@@ -476,7 +476,7 @@ int wcgh_apply_blocks(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int block,
     std::lock_guard<std::mutex> lk(ctx->mu);
     use_device(ctx);
     cudaStream_t s = ctx->stream;
-    const size_t span = size_t(2 * n - 1), n2 = size_t(n) * n;
+    const size_t n2 = size_t(n) * n;
     float2* lut = lut_in_alloc(ctx->b_lut, n, s);
     launch_build_lut(*scene, n, block, lut, ctx->b_lut_scratch, s);
     const size_t wbytes = ((dense.size() * 4 + 255) / 256) * 256;
@@ -511,7 +511,6 @@ int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, 
     cudaStream_t s = ctx->stream;
     const int mr = 2 * m;
     const size_t m2 = size_t(m) * m, r2 = size_t(mr) * mr, n2 = size_t(n) * n;
-    const size_t span = size_t(2 * n - 1);
     float2* lut = lut_in_alloc(ctx->b_lut, n, s);
     launch_build_lut(*scene, n, block, lut, ctx->b_lut_scratch, s);
     char* in = static_cast<char*>(ctx->b_in.reserve((3 * m2 + r2) * 8));
@@ -584,7 +583,6 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
       // separately from synthesis, like the reference's lut_build).
       j->w_stage.reserve(sizeof(float) * wstage_len(No) * L);
       j->stage_planes.reserve(sizeof(float2) * size_t(d.rows) * d.plane_size * 4);
-      const size_t span = size_t(2 * d.plane_size - 1);
       const int blocks[4] = {8, 4, 2, 1};
       for (int l = 0; l < L; ++l) {
         for (int st = 0; st < 4; ++st) {
