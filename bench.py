@@ -460,28 +460,36 @@ def main():
                      "issues 2 MUFU + ~15 FMA/ALU per update; not an HBM or tensor-core kernel")
             bound = "sfu"
             dram = int(points * 16 + rows * c.plane_size * 8)
-        else:
-            per_clk, kernel = 128.0 / 2.0, "k_lut_superpose (K4), 4 stage launches"
+        elif job.spec.method == "lut":
+            per_clk, kernel = 128.0 / 2.0, "k_lut_stage (K4), 4 stage launches"
             basis = (f"FP32 roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz x 128 FFMA/clk/SM / 2 FFMA per "
                      "(nonzero cell, pixel) update (SURVEY.md §8(d))")
             bound = "fp32"
             dram = int(4 * (2 * c.plane_size - 1) ** 2 * 8 + rows * c.plane_size * 8)
-        peak = SM_COUNT * f_max * per_clk
+        else:  # fft: cuFFT transforms dominate (library code, like cuBLAS)
+            per_clk, kernel = None, "cuFFT C2C on the 2Nh grid + k_spec_mul/k_scatter/k_extract"
+            basis = ("FFT method: the transforms are cuFFT (library); no hand-written-kernel roofline "
+                     "is claimed — `value` keeps the direct method's numerator")
+            bound = "hbm"
+            dram = int(3 * (2 * c.plane_size) ** 2 * 8 * c.n_layers + rows * c.plane_size * 8)
+        peak = SM_COUNT * f_max * per_clk if per_clk else None
         # dram__bytes_read + dram__bytes_write per launch from the committed
         # `ncu --set full` capture (profiles/, tools/profile_round.sh)
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
             tj = json.loads(tp.read_text())
-            traffic = tj.get("k_direct_fixed" if bound == "sfu" else "k_lut_stage")
+            traffic = tj.get({"sfu": "k_direct_fixed", "fp32": "k_lut_stage"}.get(bound, ""))
         roof = {
-            "bound": bound, "achieved": achieved, "peak": peak, "unit": UNIT,
-            "frac": achieved / peak, "traffic": traffic, "kernel": kernel, "kernel_ms": k_ms,
+            "bound": bound, "achieved": achieved if peak else None, "peak": peak, "unit": UNIT,
+            "frac": achieved / peak if peak else None, "traffic": traffic, "kernel": kernel,
+            "kernel_ms": k_ms,
             "traffic_note": ("bytes per launch from profiles/ncu_traffic.json (config-1 capture for K3; "
                              "config-2 stage average for K4); dominated by the fixed-order "
                              "partial-sum planes, not by point/LUT reads"),
             "peak_basis": basis,
-            "frac_at_measured_clock": (achieved / (SM_COUNT * f_meas * per_clk) if f_meas else None),
+            "frac_at_measured_clock": (achieved / (SM_COUNT * f_meas * per_clk)
+                                       if f_meas and per_clk else None),
             "dram_bytes_per_step_algorithmic": dram,
         }
         out = {
