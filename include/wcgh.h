@@ -217,6 +217,20 @@ int wcgh_job_run(wcgh_job* job);
  * cells for the LUT method) and ms_analysis; no synthesis. */
 int wcgh_job_analyze(wcgh_job* job);
 int wcgh_job_download(wcgh_job* job, float* out);
+/* Fused row-tile gather: register the full-plane buffers
+ * (plane_size x plane_size complex64, device pointers valid in this process —
+ * the other ranks' planes mapped over NVLink with CUDA IPC, and this rank's
+ * own) that every later run also writes its band into, at rows
+ * [row0, row0 + rows), from the kernel that produces the band's final values
+ * (no collective call). n_planes = 0 clears the list; at most 16. */
+int wcgh_job_set_peer_planes(wcgh_job* job, void* const* planes_dev, int n_planes);
+/* CUDA-IPC helpers for those planes: allocate a zeroed full plane on
+ * `device` and export its 64-byte IPC handle; map a peer's plane from its
+ * handle (lazy NVLink peer access); unmap; free. */
+int wcgh_ipc_alloc_plane(int device, int n, void** dev_ptr, unsigned char* handle64);
+int wcgh_ipc_open_plane(int device, const unsigned char* handle64, void** dev_ptr);
+int wcgh_ipc_close_plane(void* dev_ptr);
+int wcgh_ipc_free_plane(void* dev_ptr);
 /* A_eff of the last run or analyze (n_layers x No^2 fp32, row-major). */
 int wcgh_job_download_a_eff(wcgh_job* job, float* out);
 /* Compacted point list of the last direct-method run or analyze (row-major

@@ -85,6 +85,11 @@ _SIGS = [
     ("wcgh_job_run", C.c_int, [_VP]),
     ("wcgh_job_analyze", C.c_int, [_VP]),
     ("wcgh_job_download", C.c_int, [_VP, _VP]),
+    ("wcgh_job_set_peer_planes", C.c_int, [_VP, C.POINTER(_VP), C.c_int]),
+    ("wcgh_ipc_alloc_plane", C.c_int, [C.c_int, C.c_int, C.POINTER(_VP), C.c_char_p]),
+    ("wcgh_ipc_open_plane", C.c_int, [C.c_int, C.c_char_p, C.POINTER(_VP)]),
+    ("wcgh_ipc_close_plane", C.c_int, [_VP]),
+    ("wcgh_ipc_free_plane", C.c_int, [_VP]),
     ("wcgh_job_download_a_eff", C.c_int, [_VP, _VP]),
     ("wcgh_job_download_points", C.c_int, [_VP, _VP, C.c_int64, C.POINTER(C.c_int64)]),
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),

@@ -88,6 +88,7 @@ struct wcgh_job {
   bool ran = false;           // a run finished since the last upload
   bool stages_ready = false;  // stage_planes hold the per-stage planes of the last run
   DevBuf snap_img, snap_points;  // direct/FFT snapshots (computed on demand)
+  PeerPlanes peers;              // fused row-tile gather targets (wcgh_job_set_peer_planes)
   ~wcgh_job() {
     if (h_tot) cudaFreeHost(h_tot);
     if (h_offsets) cudaFreeHost(h_offsets);
@@ -706,11 +707,12 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
     // same hologram by FFT correlation; `updates` keeps the direct-sum count
     j->stats.updates = double(lb[L]) * double(d.rows) * double(d.plane_size);
     launches = launch_fft_synthesis(j->fft, j->a_eff.as<float>(), No, j->off, d.plane_size,
-                                    d.row0, d.rows, j->plane.as<float2>(), s, &j->timing);
+                                    d.row0, d.rows, j->plane.as<float2>(), s, &j->timing,
+                                    &j->peers);
   } else {
     launches = launch_direct(j->points.as<wcgh_point>(), lb, L, d.layers, d.plane_size, d.row0,
                              d.rows, d.phase_mode, far, max_dy, j->plane.as<float2>(), j->direct,
-                             s, &j->timing, &j->stats.updates);
+                             s, &j->timing, &j->stats.updates, &j->peers);
   }
   j->stats.synth_launches = j->timing.launches();
   j->stats.total_launches += launches;
@@ -725,7 +727,7 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
 }
 
 __global__ void k_sum_stages(const float2* __restrict__ planes, size_t count, int n_stages,
-                             float2* __restrict__ out) {
+                             float2* __restrict__ out, PeerPlanes peers) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   float re = 0.f, im = 0.f;
@@ -735,6 +737,7 @@ __global__ void k_sum_stages(const float2* __restrict__ planes, size_t count, in
     im += v.y;
   }
   out[i] = make_float2(re, im);
+  store_peers(peers, i, make_float2(re, im));  // fused row-tile gather (job run only)
 }
 
 void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
@@ -789,7 +792,8 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
     }
   j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));
-  k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(sp, band, 4, j->plane.as<float2>());
+  k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(sp, band, 4, j->plane.as<float2>(),
+                                                            j->peers);
   WCGH_CHECK_LAUNCH();
   j->stats.total_launches += 1;
   WCGH_CUDA(cudaEventRecord(j->ev[3], s));
@@ -893,6 +897,62 @@ int wcgh_job_download(wcgh_job* job, float* out) {
   });
 }
 
+int wcgh_job_set_peer_planes(wcgh_job* job, void* const* planes_dev, int n_planes) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job != nullptr, "job_set_peer_planes: NULL job");
+    require(n_planes >= 0 && n_planes <= kMaxPeers, "job_set_peer_planes: 0..16 planes");
+    require(n_planes == 0 || planes_dev != nullptr, "job_set_peer_planes: NULL plane list");
+    PeerPlanes pp{};
+    for (int k = 0; k < n_planes; ++k) {
+      require(planes_dev[k] != nullptr, "job_set_peer_planes: NULL plane pointer");
+      pp.p[k] = static_cast<float2*>(planes_dev[k]);
+    }
+    pp.n = n_planes;
+    pp.offset = size_t(job->desc.row0) * size_t(job->desc.plane_size);
+    job->peers = pp;
+  });
+}
+
+// ---- CUDA IPC for the fused gather (one process per GPU) --------------------
+
+int wcgh_ipc_alloc_plane(int device, int n, void** dev_ptr, unsigned char* handle64) {
+  return guard(nullptr, [&] {
+    require(dev_ptr && handle64, "ipc_alloc_plane: NULL argument");
+    require(n >= 1 && n <= 65536, "ipc_alloc_plane: bad plane size");
+    WCGH_CUDA(cudaSetDevice(device));
+    void* p = nullptr;
+    WCGH_CUDA(cudaMalloc(&p, sizeof(float2) * size_t(n) * size_t(n)));
+    WCGH_CUDA(cudaMemset(p, 0, sizeof(float2) * size_t(n) * size_t(n)));
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      throw RuntimeError(std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    *dev_ptr = p;
+  });
+}
+
+int wcgh_ipc_open_plane(int device, const unsigned char* handle64, void** dev_ptr) {
+  return guard(nullptr, [&] {
+    require(dev_ptr && handle64, "ipc_open_plane: NULL argument");
+    WCGH_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    WCGH_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int wcgh_ipc_close_plane(void* dev_ptr) {
+  return guard(nullptr, [&] { WCGH_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
+}
+
+int wcgh_ipc_free_plane(void* dev_ptr) {
+  return guard(nullptr, [&] { WCGH_CUDA(cudaFree(dev_ptr)); });
+}
+
 int wcgh_job_download_a_eff(wcgh_job* job, float* out) {
   return guard(job ? job->ctx : nullptr, [&] {
     require(job && out, "job_download_a_eff: NULL argument");
@@ -932,7 +992,7 @@ int wcgh_job_download_stages(wcgh_job* job, float* out4) {
     for (int st = 0; st < 4; ++st) {
       // snapshot after stage st = sum of stage planes 0..st, in stage order
       k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(job->stage_planes.as<float2>(), band,
-                                                                st + 1, tmp);
+                                                                st + 1, tmp, PeerPlanes{});
       WCGH_CHECK_LAUNCH();
       WCGH_CUDA(cudaMemcpyAsync(out4 + 2 * band * st, tmp, sizeof(float2) * band, cudaMemcpyDeviceToHost, s));
       sync(s);

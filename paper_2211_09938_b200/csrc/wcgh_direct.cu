@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads)
 // Fixed-order chunk reduction: out (+)= sum_c partial[c], c in chunk order,
 // accumulated in fp64.
 __global__ void k_reduce_chunks(const float2* __restrict__ partial, int n_chunks, size_t count,
-                                int accumulate, float2* __restrict__ out) {
+                                int accumulate, float2* __restrict__ out, PeerPlanes peers) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double re = 0.0, im = 0.0;
@@ -234,7 +234,14 @@ __global__ void k_reduce_chunks(const float2* __restrict__ partial, int n_chunks
     re += v.x;
     im += v.y;
   }
-  out[i] = make_float2(float(re), float(im));
+  const float2 r = make_float2(float(re), float(im));
+  out[i] = r;
+  store_peers(peers, i, r);  // fused row-tile gather (last chunk group only)
+}
+
+__global__ void k_band_to_peers(const float2* __restrict__ band, size_t count, PeerPlanes peers) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) store_peers(peers, i, band[i]);
 }
 
 // binom(a, n) for real a.
@@ -364,7 +371,8 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
 int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
-                  cudaStream_t stream, DirectTiming* timing, double* updates_out) {
+                  cudaStream_t stream, DirectTiming* timing, double* updates_out,
+                  const PeerPlanes* peers) {
   require(n_layers >= 1 && n_layers <= kMaxLayers, "direct: 1..16 layers");
   require(rows >= 1 && row0 >= 0 && row0 + rows <= nh, "direct: row band outside the plane");
   require(phase_mode == WCGH_PHASE_FIXED || phase_mode == WCGH_PHASE_FP64,
@@ -374,6 +382,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
   const size_t band = size_t(rows) * nh;
   if (n_points == 0) {
     WCGH_CUDA(cudaMemsetAsync(out_dev, 0, band * sizeof(float2), stream));
+    if (peers && peers->n) return launch_band_to_peers(out_dev, band, *peers, stream);
     return 0;
   }
   DirectPlan plan{};
@@ -420,12 +429,21 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     }
     WCGH_CHECK_LAUNCH();
     if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), stream));
-    k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(partial, ng, band, g0 > 0,
-                                                                      out_dev);
+    const bool last = g0 + ng >= n_chunks;
+    k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(
+        partial, ng, band, g0 > 0, out_dev, last && peers ? *peers : PeerPlanes{});
     WCGH_CHECK_LAUNCH();
     launches += 2;
   }
   return launches;
+}
+
+int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes& peers,
+                         cudaStream_t stream) {
+  if (peers.n == 0 || count == 0) return 0;
+  k_band_to_peers<<<unsigned((count + 255) / 256), 256, 0, stream>>>(band_dev, count, peers);
+  WCGH_CHECK_LAUNCH();
+  return 1;
 }
 
 }  // namespace wcgh

@@ -73,12 +73,14 @@ __global__ void k_spec_mul(const float2* __restrict__ fa, const float2* __restri
 
 // out (rows x nh) = grid[row0 + y][x] / L^2.
 __global__ void k_extract(const float2* __restrict__ grid, int L, int nh, int row0, int rows,
-                          float scale, float2* __restrict__ out) {
+                          float scale, float2* __restrict__ out, PeerPlanes peers) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= size_t(rows) * nh) return;
   const int x = int(i % nh), y = int(i / nh);
   const float2 v = grid[size_t(row0 + y) * L + x];
-  out[i] = make_float2(v.x * scale, v.y * scale);
+  const float2 r = make_float2(v.x * scale, v.y * scale);
+  out[i] = r;
+  store_peers(peers, i, r);  // fused row-tile gather
 }
 
 inline unsigned blocks_for(size_t n) { return unsigned((n + 255) / 256); }
@@ -120,7 +122,8 @@ void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cu
 }
 
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
-                         int rows, float2* out, cudaStream_t s, DirectTiming* timing) {
+                         int rows, float2* out, cudaStream_t s, DirectTiming* timing,
+                         const PeerPlanes* peers) {
   const int L = fp.L;
   const size_t L2 = size_t(L) * L;
   WCGH_CUFFT(cufftSetStream(fp.plan, s));
@@ -145,7 +148,8 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
                           reinterpret_cast<cufftComplex*>(acc), CUFFT_INVERSE));
   dbg(s, "inverse_fft");
   k_extract<<<blocks_for(size_t(rows) * nh), 256, 0, s>>>(acc, L, nh, row0, rows,
-                                                          float(1.0 / double(L2)), out);
+                                                          float(1.0 / double(L2)), out,
+                                                          peers ? *peers : PeerPlanes{});
   WCGH_CHECK_LAUNCH();
   if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
   return launches + 2;

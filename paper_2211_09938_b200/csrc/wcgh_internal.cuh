@@ -63,6 +63,26 @@ struct DevBuf {
   }
 };
 
+// ---- fused row-tile gather -------------------------------------------------
+// Full-plane buffers of every rank (device pointers valid in this process,
+// e.g. CUDA-IPC-mapped over NVLink): the kernel that produces a band's final
+// values also stores each value into every listed plane at its global
+// position (offset = row0 * Nh elements), so the all-gather rides on the
+// epilogue's stores instead of a separate collective.
+constexpr int kMaxPeers = 16;
+struct PeerPlanes {
+  float2* p[kMaxPeers];
+  int n = 0;
+  size_t offset = 0;
+};
+__device__ __forceinline__ void store_peers(const PeerPlanes& pp, size_t i, float2 v) {
+  for (int k = 0; k < pp.n; ++k) pp.p[k][pp.offset + i] = v;
+}
+
+// copy a finished band into the peer planes (used where no fused epilogue exists)
+int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes& peers,
+                         cudaStream_t stream);
+
 // ---- direct accumulation (K3) ---------------------------------------------
 
 constexpr int kMaxLayers = 16;
@@ -137,7 +157,8 @@ struct DirectScratch {
 int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
-                  cudaStream_t stream, DirectTiming* timing, double* updates_out);
+                  cudaStream_t stream, DirectTiming* timing, double* updates_out,
+                  const PeerPlanes* peers = nullptr);
 
 // ---- analysis (K1 + K2) ----------------------------------------------------
 
@@ -222,7 +243,8 @@ struct FftPlan {
 void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cudaStream_t stream);
 // out (rows x nh) = band of sum_layers A_eff_l (*) F_l.
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
-                         int rows, float2* out, cudaStream_t stream, DirectTiming* timing);
+                         int rows, float2* out, cudaStream_t stream, DirectTiming* timing,
+                         const PeerPlanes* peers = nullptr);
 
 // ---- reconstruction and SSIM (K6, K7) --------------
 struct ReconPlan {

@@ -151,6 +151,12 @@ class HologramJob:
         lut = np.ascontiguousarray(lut, np.complex64)
         L.check(self.ctx.lib.wcgh_job_load_lut(self.h, int(layer), int(block), L.ptr(lut)))
 
+    def set_peer_planes(self, ptrs) -> None:
+        """Fused row-tile gather: device pointers of full planes (this rank's and
+        the IPC-mapped peers') that every run also writes its band into."""
+        arr = (C.c_void_p * max(1, len(ptrs)))(*[C.c_void_p(int(p)) for p in ptrs])
+        L.check(self.ctx.lib.wcgh_job_set_peer_planes(self.h, arr, len(ptrs)))
+
     def plane_dev_ptr(self) -> int:
         return int(self.ctx.lib.wcgh_job_plane_dev(self.h) or 0)
 

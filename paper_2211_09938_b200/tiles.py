@@ -1,7 +1,9 @@
 """Multi-GPU decomposition: contiguous row bands of the hologram plane, one
 per rank (one process per GPU), every rank seeing the full compacted point
-list; the only exchange is one all-gather of the row tiles (NCCL over
-NVLink/NVSwitch on B200 boxes, gloo in the CPU tests). Row-major bands are
+list; the only exchange is the all-gather of the row tiles — fused into the
+band's final kernel as NVLink P2P stores into CUDA-IPC-mapped peer planes
+(PeerPlaneExchange), or as an NCCL all-gather (gather_tiles; gloo in the CPU
+tests). Row-major bands are
 contiguous, so the gathered buffer is the plane with no repacking. The
 per-pixel summation order does not depend on the band split (see
 csrc/wcgh_direct.cu), so the gathered plane is bitwise identical for any
@@ -65,6 +67,60 @@ def gather_tiles(tile, world: int, plane_size: int, out=None):
         out = torch.empty((plane_size, tile.shape[1]), dtype=tile.dtype, device=tile.device)
     dist.all_gather_into_tensor(out, tile.contiguous())
     return out
+
+
+class PeerPlaneExchange:
+    """Fused row-tile gather over NVLink (one process per GPU): every rank
+    allocates its full plane with an exported CUDA IPC handle, the handles
+    are all-gathered once (host objects, any torch.distributed backend), and
+    each rank maps its peers' planes. A job registered with `register` then
+    writes its band into every rank's plane from the epilogue of the kernel
+    that produces it (wcgh_job_set_peer_planes) — no collective per step; a
+    barrier tells the ranks when all bands have landed."""
+
+    def __init__(self, world: int, rank: int, plane_size: int, device: int):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib as L
+
+        self.lib = L.load()
+        self.n, self.world, self.rank, self.device = plane_size, world, rank, device
+        own = C.c_void_p()
+        handle = C.create_string_buffer(64)
+        L.check(self.lib.wcgh_ipc_alloc_plane(device, plane_size, C.byref(own), handle))
+        self.own = int(own.value)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle.raw)
+        self.ptrs, self.opened = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                self.ptrs.append(self.own)
+                continue
+            p = C.c_void_p()
+            L.check(self.lib.wcgh_ipc_open_plane(device, h, C.byref(p)))
+            self.ptrs.append(int(p.value))
+            self.opened.append(int(p.value))
+
+    def register(self, job) -> None:
+        job.set_peer_planes(self.ptrs)
+
+    def plane_tensor(self):
+        """torch (Nh, 2*Nh) float32 view of this rank's assembled plane."""
+        import torch
+
+        return torch.as_tensor(CudaView(self.own, (self.n, 2 * self.n)), device="cuda")
+
+    def close(self) -> None:
+        import ctypes as C
+
+        for p in self.opened:
+            self.lib.wcgh_ipc_close_plane(C.c_void_p(p))
+        self.opened = []
+        if self.own:
+            self.lib.wcgh_ipc_free_plane(C.c_void_p(self.own))
+            self.own = 0
 
 
 def as_complex(plane_f32) -> np.ndarray:
