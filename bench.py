@@ -344,9 +344,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank path on a single GPU only (numbers
+    # from such a run are not measurements): all ranks on device 0, gloo
+    if os.environ.get("WCGH_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("WCGH_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     sc = scenes.make_scene(args.config)
     c = sc.config
     row0, rows = tiles.band(rank, world, c.plane_size)
@@ -368,14 +376,27 @@ def main():
     full_h = torch.empty((c.plane_size, 2 * c.plane_size), dtype=torch.float32).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    gathered = None
+    # multi-GPU: the row-tile all-gather is fused into the band's final kernel
+    # (NVLink P2P stores into CUDA-IPC-mapped peer planes); NCCL all-gather
+    # only if the IPC mapping cannot be set up on this box
+    gathered, exchange, gather_mode = None, None, "none (1 GPU)"
     if world > 1:
-        gathered = torch.empty((c.plane_size, 2 * c.plane_size), dtype=torch.float32, device="cuda")
+        try:
+            exchange = tiles.PeerPlaneExchange(world, rank, c.plane_size, local)
+            exchange.register(job)
+            gather_mode = "fused: band epilogue stores into CUDA-IPC peer planes over NVLink"
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            gather_mode = f"NCCL all_gather_into_tensor (IPC peer planes unavailable: {e})"
+            gathered = torch.empty((c.plane_size, 2 * c.plane_size), dtype=torch.float32,
+                                   device="cuda")
 
     def step():
         job.run()
         if world > 1:
-            tiles.gather_tiles(tiles.tile_tensor(job), world, c.plane_size, out=gathered)
+            if exchange is not None:
+                dist.barrier()  # every rank's band has landed in every plane
+            else:
+                tiles.gather_tiles(tiles.tile_tensor(job), world, c.plane_size, out=gathered)
 
     job.upload_dev(obj_d.data_ptr(), sal_d.data_ptr())
     for _ in range(args.warmup):
@@ -426,9 +447,14 @@ def main():
         job.upload(obj_h.numpy(), sal_h.numpy())
         job.run()
         if world > 1:
-            tiles.gather_tiles(tiles.tile_tensor(job), world, c.plane_size, out=gathered)
-            if rank == 0:
-                full_h.copy_(gathered)
+            if exchange is not None:
+                dist.barrier()
+                if rank == 0:
+                    full_h.copy_(exchange.plane_tensor())
+            else:
+                tiles.gather_tiles(tiles.tile_tensor(job), world, c.plane_size, out=gathered)
+                if rank == 0:
+                    full_h.copy_(gathered)
         else:
             job.download(full_h.numpy().view(np.complex64))
         torch.cuda.synchronize()
@@ -501,6 +527,7 @@ def main():
                        "layers": c.n_layers, "points": points, "updates_per_hologram": updates,
                        "method": job.spec.method, "phase": "fixed-point quadratic + fp32 series",
                        "ops": stats["ops"], "parallelism": f"row tiles x{world}",
+                       "gather": gather_mode,
                        "l2": "flushed between timed steps (256 MiB write, outside the step interval)"},
             "ms_per_hologram": ms_per_step,
             "precompute_ms": precompute_ms,
@@ -563,6 +590,10 @@ def main():
                 out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                                        "sample": f"failed: {e}"}
         print(json.dumps(out))
+    if world > 1:
+        dist.barrier()  # no rank unmaps / frees a plane another rank still writes
+    if exchange is not None:
+        exchange.close()
     job.close()
     ctx.close()
     if world > 1:
