@@ -87,21 +87,41 @@ class PeerPlaneExchange:
 
         self.lib = L.load()
         self.n, self.world, self.rank, self.device = plane_size, world, rank, device
-        own = C.c_void_p()
-        handle = C.create_string_buffer(64)
-        L.check(self.lib.wcgh_ipc_alloc_plane(device, plane_size, C.byref(own), handle))
-        self.own = int(own.value)
+        self.own, self.ptrs, self.opened = 0, [], []
+        # every step is agreed on by all ranks, so a failure on one rank makes
+        # all of them raise (and fall back) instead of leaving some blocked
+        handle = None
+        try:
+            own = C.c_void_p()
+            buf = C.create_string_buffer(64)
+            L.check(self.lib.wcgh_ipc_alloc_plane(device, plane_size, C.byref(own), buf))
+            self.own, handle = int(own.value), buf.raw
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank}: {e}"
         handles = [None] * world
-        dist.all_gather_object(handles, handle.raw)
-        self.ptrs, self.opened = [], []
-        for r, h in enumerate(handles):
-            if r == rank:
-                self.ptrs.append(self.own)
-                continue
-            p = C.c_void_p()
-            L.check(self.lib.wcgh_ipc_open_plane(device, h, C.byref(p)))
-            self.ptrs.append(int(p.value))
-            self.opened.append(int(p.value))
+        dist.all_gather_object(handles, handle)
+        if any(h is None for h in handles):
+            self.close()
+            raise RuntimeError("peer planes: IPC allocation failed on some rank"
+                               + (f" ({err})" if handle is None else ""))
+        ok = True
+        try:
+            for r, h in enumerate(handles):
+                if r == rank:
+                    self.ptrs.append(self.own)
+                    continue
+                p = C.c_void_p()
+                L.check(self.lib.wcgh_ipc_open_plane(device, h, C.byref(p)))
+                self.ptrs.append(int(p.value))
+                self.opened.append(int(p.value))
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, f"rank {rank}: {e}"
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if not all(oks):
+            self.close()
+            raise RuntimeError("peer planes: IPC mapping failed on some rank"
+                               + (f" ({err})" if not ok else ""))
 
     def register(self, job) -> None:
         job.set_peer_planes(self.ptrs)
