@@ -77,3 +77,30 @@ def test_row_tiles_gather_equals_single_rank(tmp_path, world):
     single = _band_hologram(n, pts, layers, 0, n)
     assert gathered.shape == (n, n)
     assert np.array_equal(gathered, single)
+
+
+def _exchange_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    msg = "ok"
+    try:
+        tiles.PeerPlaneExchange(world, rank, 64, 0)
+    except RuntimeError as e:
+        msg = str(e)
+    with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
+        f.write(msg)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_plane_exchange_fails_consistently_without_gpu(tmp_path):
+    """The fused-gather setup agrees on every step across ranks: with no GPU
+    (IPC allocation fails everywhere) every rank raises, none is left blocked
+    in a collective, so bench.py can fall back together."""
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a GPU")
+    mp.spawn(_exchange_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        msg = (tmp_path / f"r{r}.txt").read_text()
+        assert "IPC allocation failed" in msg, msg
