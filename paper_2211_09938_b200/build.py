@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "wcgh"
 LIB = PKG / "libwcgh.so"
 SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_fft.cu", "wcgh_recon.cu",
-           "wcgh_abi.cu"]
+           "wcgh_abi.cu", "wcgh_job.cu", "wcgh_io.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -34,7 +34,8 @@ def _run(cmd: list[str], log: Path | None = None) -> None:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
-    deps = [CSRC / s for s in SOURCES] + [CSRC / "wcgh_internal.cuh", ROOT / "include" / "wcgh.h"]
+    deps = [CSRC / s for s in SOURCES] + [CSRC / "wcgh_internal.cuh", CSRC / "wcgh_state.cuh",
+                                           ROOT / "include" / "wcgh.h"]
     newest = max(p.stat().st_mtime for p in deps)
     if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
         return LIB
