@@ -282,6 +282,26 @@ class ReferenceTimer:
         return est, desc, self.workers
 
 
+def reference_direct_rate():
+    """The reference's own direct Eq.(1) (pointwise_hologram_reference,
+    tests/support/oracles.cpp:12-36 — the formula K3 evaluates), single
+    thread, on a seeded 64^2 object: updates/s (SURVEY.md §8(d) direct-formula
+    baseline)."""
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return None
+    n = 64
+    amp = np.random.default_rng(64).random((n, n))
+    t0 = time.perf_counter()
+    O.ref_pointwise_hologram_reference(amp, 532e-9, 8e-6, 0.2)
+    dt = time.perf_counter() - t0
+    upd = float(np.count_nonzero(amp)) * n * n
+    return {"value": upd / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"pointwise_hologram_reference on a {n}^2 object / {n}^2 plane, 1 thread, "
+                      f"{dt:.2f} s"}
+
+
 def reference_cpu_sample(scene, target_seconds: float = 10.0):
     t = ReferenceTimer(scene)
     try:
@@ -586,6 +606,7 @@ def main():
                 cb = reference_cpu_sample(sc, target_seconds=args.cpu_seconds)
                 out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
                 out["cpu_baseline"]["ms_per_hologram"] = cb["ms_per_hologram"]
+                out["cpu_baseline_direct_formula"] = reference_direct_rate()
             except Exception as e:  # the baseline is reported, never required
                 out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                                        "sample": f"failed: {e}"}
