@@ -40,8 +40,11 @@ extern "C" {
 enum { WCGH_OK = 0, WCGH_EVALIDATION = 1, WCGH_ERUNTIME = 2 };
 
 /* Input sample types. U8 objects are amplitudes v * obj_scale; U8 saliency is
- * v * (1/255), the reference loader's scale_to_unit (image_io.cpp:177-190). */
-enum { WCGH_U8 = 0, WCGH_F32 = 1, WCGH_F64 = 2 };
+ * v * (1/255), the reference loader's scale_to_unit (image_io.cpp:177-190).
+ * C128 (job objects only) is an interleaved complex<double> amplitude, the
+ * random-initial-phase object of synthesize_progressive(..., seed)
+ * (synthesis.cpp:205-219; make it with wcgh_random_phase_field). */
+enum { WCGH_U8 = 0, WCGH_F32 = 1, WCGH_F64 = 2, WCGH_C128 = 3 };
 
 /* Synthesis method. DIRECT evaluates Eq.(1) per (point, pixel) on the SFU
  * (tests/support/oracles.cpp:12-36 applied to the effective amplitude);
@@ -237,6 +240,11 @@ int wcgh_job_download_a_eff(wcgh_job* job, float* out);
  * ascending per layer): *n_out = count; copies it when out != NULL and
  * capacity >= count. */
 int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, int64_t* n_out);
+/* Complex-object jobs (obj_dtype WCGH_C128): the imaginary parts matching
+ * wcgh_job_download_a_eff / wcgh_job_download_points (whose values are the
+ * real parts; a point is kept when either part is nonzero). */
+int wcgh_job_download_a_eff_im(wcgh_job* job, float* out);
+int wcgh_job_download_points_im(wcgh_job* job, float* out, int64_t capacity);
 /* Stage snapshots of the last run: base_LLL, after_LL, after_L, after_full
  * (synthesis.hpp:43-54), each rows x Nh complex64. The LUT method keeps its
  * stage planes from the run; the direct and FFT methods synthesise the four
@@ -245,6 +253,14 @@ int wcgh_job_download_stages(wcgh_job* job, float* out4);
 /* Device pointer of the row band (rows x Nh complex64), valid until destroy. */
 void* wcgh_job_plane_dev(wcgh_job* job);
 int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out);
+
+/* Replaces random_phase_field (synthesis.hpp:101-104, synthesis.cpp:288-296):
+ * out[i] = polar(amplitude[i], U[0, 2pi)) with std::mt19937_64(seed) drawn
+ * in sample order — the reference's own sequential host RNG (libstdc++), so
+ * the complex object is bit-identical. HOST function: no device work.
+ * out: width x height interleaved complex128, the WCGH_C128 object layout. */
+int wcgh_random_phase_field(const double* amplitude, int width, int height, uint64_t seed,
+                            double* out);
 
 /* ---- CGH1 hologram files (image_io.cpp:220-278) --------------
  * "CGH1", u16 version = 1, u32 N, f64 wavelength, f64 pitch, f64 z (little

@@ -24,7 +24,9 @@ int ref_synthesize_progressive(const double* object, const double* saliency, int
                                const int* enables, int workers, int use_seed, std::uint64_t seed,
                                double* planes_out, std::uint8_t* masks_out, std::uint64_t* ops_out);
 int ref_synthesize_pointwise_oracle(const double* object, int n, double wl, double pitch, double z,
-                                    int workers, double* out, std::uint64_t* ops);
+                                    int workers, int use_seed, std::uint64_t seed, double* out,
+                                    std::uint64_t* ops);
+int ref_random_phase_field(const double* amp, int n, std::uint64_t seed, double* out);
 int ref_random_image(int w, int h, std::uint64_t seed, double* out);
 int ref_build_block_lut(double wl, double pitch, double z, int n, int block, int workers, double* out);
 int ref_reconstruct(const double* holo, int n, double wl, double pitch, double z, int intensity,
@@ -112,9 +114,30 @@ int main() {
     OpCounter pc;
     const ComplexField pw = synthesize_pointwise_oracle(object, scene, pc, luts.of(1));
     std::uint64_t pops = 0;
-    ref_synthesize_pointwise_oracle(object.data().data(), n, wl, pitch, z, 1, planes.data(), &pops);
+    ref_synthesize_pointwise_oracle(object.data().data(), n, wl, pitch, z, 1, 0, 0, planes.data(), &pops);
     EXPECT(rel_l2(pw, planes.data()) <= 1e-4, "pointwise oracle n=%d", n);
     EXPECT(pc.get(OpLevel::kPointwiseOracle) == pops, "pointwise ops n=%d", n);
+
+    // random initial phase (synthesis.cpp:205-219, 269-284, 288-296)
+    const std::uint64_t seed = 424242 + n;
+    const ComplexField rot = random_phase_field(object, seed);
+    std::vector<double> rref(std::size_t(2) * n * n);
+    ref_random_phase_field(object.data().data(), n, seed, rref.data());
+    EXPECT(std::memcmp(rot.data().data(), rref.data(), rref.size() * 8) == 0,
+           "random_phase_field n=%d not bit-identical", n);
+    const ProgressiveResult rp = synthesize_progressive(object, saliency, scene, plan, luts, 1, seed);
+    ref_synthesize_progressive(object.data().data(), saliency.data().data(), n, wl, pitch, z, th, en,
+                               1, 1, seed, planes.data(), masks.data(), ops);
+    for (int s = 0; s < 4; ++s) {
+      const double e = rel_l2(rp.stage(s), planes.data() + std::size_t(2) * n * n * s);
+      EXPECT(e <= 1e-4, "random phase n=%d stage %d rel L2 %.3e", n, s, e);
+    }
+    for (int i = 0; i < 5; ++i) EXPECT(rp.ops.get(kAllOpLevels[i]) == ops[i], "random phase ops[%d] n=%d", i, n);
+    OpCounter pc2;
+    const ComplexField pw2 = synthesize_pointwise_oracle(object, scene, pc2, luts.of(1), 1, seed);
+    ref_synthesize_pointwise_oracle(object.data().data(), n, wl, pitch, z, 1, 1, seed, planes.data(), &pops);
+    EXPECT(rel_l2(pw2, planes.data()) <= 1e-4, "pointwise oracle (random phase) n=%d", n);
+    EXPECT(pc2.get(OpLevel::kPointwiseOracle) == pops, "pointwise ops (random phase) n=%d", n);
 
     // apply_block with a complex weight (synthesis.cpp:37-41)
     ComplexField plane(n, n);

@@ -14,8 +14,11 @@
 //  * planes are computed in complex64 on the device and widened to the
 //    reference's complex<double> (relative L2 ~1e-6 vs the fp64 reference);
 //  * `workers` is accepted and ignored (results are launch-invariant);
-//  * random_phase_seed is rejected (complex amplitudes are out of scope,
-//    DESIGN.md §7); random_phase_field itself stays a host RNG function;
+//  * random_phase_seed: random_phase_field draws the phases on the host with
+//    the reference's engine (bit-identical complex object); the complex
+//    object is then analysed and synthesised part by part on the device
+//    (WCGH_C128 jobs; the direct method folds the phase into its fixed-point
+//    phase, the LUT method superposes i * the imaginary weights);
 //  * build_block_lut runs on the device (K5: fp64 sums, complex64 store — the
 //    CGHL payload precision) and is widened to the FringeLut's
 //    complex<double>; lut_cache_store/load go through the ABI's CGHL I/O;
@@ -28,8 +31,7 @@
 #include <complex>
 #include <cstring>
 #include <mutex>
-#include <numbers>
-#include <random>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -300,13 +302,14 @@ int method_code(SynthesisMethod m) {
 ProgressiveResult run_progressive(const std::vector<const RealImage*>& objects,
                                   const std::vector<const RealImage*>& saliencies,
                                   const std::vector<SceneParams>& scenes, const RefinementPlan& plan,
-                                  int method) {
+                                  int method, std::optional<std::uint64_t> seed = {}) {
   plan.validate();
   const int L = int(scenes.size());
   if (L < 1 || int(objects.size()) != L || int(saliencies.size()) != L)
     throw ValidationError("synthesize_progressive: one object and saliency per layer");
   const int n = scenes[0].plane_size();
   if (n < 8) throw ValidationError("synthesize_progressive: plane_size must be >= 8");
+  if (seed && L != 1) throw ValidationError("synthesize_progressive: random phase needs one layer");
   std::vector<wcgh_layer> layers;
   std::vector<double> obj, sal;
   for (int l = 0; l < L; ++l) {
@@ -334,6 +337,12 @@ ProgressiveResult run_progressive(const std::vector<const RealImage*>& objects,
   d.obj_dtype = WCGH_F64;
   d.obj_scale = 1.0;
   d.sal_dtype = WCGH_F64;
+  if (seed) {  // synthesis.cpp:205-214: the complex object, interleaved (re, im)
+    std::vector<double> rotated(2 * obj.size());
+    check(wcgh_random_phase_field(obj.data(), n, n, *seed, rotated.data()));
+    obj.swap(rotated);
+    d.obj_dtype = WCGH_C128;
+  }
   wcgh_job* job = nullptr;
   check(wcgh_job_create(gpu(), &d, &job));
   std::vector<float> stages(std::size_t(8) * n * n);
@@ -387,10 +396,8 @@ ProgressiveResult synthesize_progressive(const RealImage& object, const RealImag
       throw ValidationError("synthesize_progressive: missing LUT for block size " + std::to_string(b));
   if (!(luts.of(1).scene() == scene))
     throw ValidationError("synthesize_progressive: LUTs built for a different scene");
-  if (random_phase_seed)
-    throw ValidationError("synthesize_progressive: random initial phase is not supported by the GPU path");
   // the reference's algorithm (its LutSet argument)
-  return run_progressive({&object}, {&saliency}, {scene}, plan, WCGH_METHOD_LUT);
+  return run_progressive({&object}, {&saliency}, {scene}, plan, WCGH_METHOD_LUT, random_phase_seed);
 }
 
 ProgressiveResult synthesize_progressive(const RealImage& object, const RealImage& saliency,
@@ -419,30 +426,39 @@ ComplexField synthesize_pointwise_oracle(const RealImage& object, const ScenePar
     throw ValidationError("pointwise oracle: object size does not match the scene");
   if (unit_lut.block_size() != 1) throw ValidationError("pointwise oracle: needs the 1x1 LUT");
   if (!(unit_lut.scene() == scene)) throw ValidationError("pointwise oracle: LUT built for a different scene");
-  if (random_phase_seed)
-    throw ValidationError("pointwise oracle: random initial phase is not supported by the GPU path");
   // every object pixel through the 1x1 LUT = the B=1 superposition of all pixels
   const wcgh_layer L = layer_of(scene);
   std::vector<uint32_t> cells(std::size_t(n) * n);
   std::vector<float> w(cells.size());
   for (std::size_t i = 0; i < cells.size(); ++i) {
     cells[i] = uint32_t(i);
-    w[i] = float(object.data()[i]);
     if (!std::isfinite(object.data()[i])) throw ValidationError("object: non-finite sample");
   }
+  std::optional<ComplexField> rotated;
+  if (random_phase_seed) rotated = random_phase_field(object, *random_phase_seed);
+  for (std::size_t i = 0; i < cells.size(); ++i)
+    w[i] = float(rotated ? rotated->data()[i].real() : object.data()[i]);
   std::vector<float> c(2 * cells.size(), 0.0f);
   uint64_t ops = 0;
   check(wcgh_apply_blocks(gpu(), &L, n, 1, cells.data(), w.data(), int64_t(cells.size()), c.data(), &ops));
   counter.add(OpLevel::kPointwiseOracle, ops);
-  return widen(c, n);
+  ComplexField out = widen(c, n);
+  if (rotated) {  // complex weights (synthesis.cpp:269-284): + i * the imaginary superposition
+    for (std::size_t i = 0; i < cells.size(); ++i) w[i] = float(rotated->data()[i].imag());
+    std::fill(c.begin(), c.end(), 0.0f);
+    uint64_t ops_im = 0;
+    check(wcgh_apply_blocks(gpu(), &L, n, 1, cells.data(), w.data(), int64_t(cells.size()), c.data(), &ops_im));
+    for (std::size_t i = 0; i < cells.size(); ++i)
+      out.data()[i] += std::complex<double>(-double(c[2 * i + 1]), double(c[2 * i]));
+  }
+  return out;
 }
 
 ComplexField random_phase_field(const RealImage& amplitude, std::uint64_t seed) {
-  // host RNG, identical to the reference (synthesis.cpp:288-296)
-  std::mt19937_64 rng(seed);
-  std::uniform_real_distribution<double> angle(0.0, 2.0 * std::numbers::pi);
+  // host RNG through the library, identical to the reference (synthesis.cpp:288-296)
   ComplexField out(amplitude.width(), amplitude.height());
-  for (std::size_t i = 0; i < out.size(); ++i) out.data()[i] = std::polar(amplitude.data()[i], angle(rng));
+  check(wcgh_random_phase_field(amplitude.data().data(), amplitude.width(), amplitude.height(), seed,
+                                reinterpret_cast<double*>(out.data().data())));
   return out;
 }
 

@@ -338,23 +338,37 @@ def ref_synthesize_progressive(obj, sal, wl, pitch, z, t=(0.5, 0.7, 0.9), en=(1,
     return planes, masks, ops
 
 
-def ref_pointwise_oracle(obj, wl, pitch, z, workers=0):
+def ref_pointwise_oracle(obj, wl, pitch, z, workers=0, seed=None):
     obj = np.ascontiguousarray(obj, np.float64)
     n = obj.shape[0]
     out = np.empty((n, n), np.complex128)
     ops = C.c_uint64()
     _ref_check(ref().ref_synthesize_pointwise_oracle(_p(obj), C.c_int(n), C.c_double(wl),
                                                      C.c_double(pitch), C.c_double(z),
-                                                     C.c_int(workers), _p(out), C.byref(ops)))
+                                                     C.c_int(workers), C.c_int(seed is not None),
+                                                     C.c_uint64(seed or 0), _p(out), C.byref(ops)))
     return out, int(ops.value)
 
 
 def ref_pointwise_hologram_reference(amp, wl, pitch, z):
+    """amp real (float64) or complex (complex128)."""
+    amp = np.asarray(amp)
+    n = amp.shape[0]
+    out = np.empty((n, n), np.complex128)
+    re = np.ascontiguousarray(amp.real, np.float64)
+    im = np.ascontiguousarray(amp.imag, np.float64) if np.iscomplexobj(amp) else None
+    _ref_check(ref().ref_pointwise_hologram_reference(_p(re), _p(im) if im is not None else None,
+                                                      C.c_int(n), C.c_double(wl),
+                                                      C.c_double(pitch), C.c_double(z), _p(out)))
+    return out
+
+
+def ref_random_phase_field(amp, seed):
+    """random_phase_field (synthesis.cpp:288-296) of the reference itself."""
     amp = np.ascontiguousarray(amp, np.float64)
     n = amp.shape[0]
     out = np.empty((n, n), np.complex128)
-    _ref_check(ref().ref_pointwise_hologram_reference(_p(amp), None, C.c_int(n), C.c_double(wl),
-                                                      C.c_double(pitch), C.c_double(z), _p(out)))
+    _ref_check(ref().ref_random_phase_field(_p(amp), C.c_int(n), C.c_uint64(seed), _p(out)))
     return out
 
 

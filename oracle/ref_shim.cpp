@@ -187,14 +187,17 @@ int ref_synthesize_progressive(const double* object, const double* saliency, int
   });
 }
 
-// synthesize_pointwise_oracle (synthesis.cpp:255-286).
+// synthesize_pointwise_oracle (synthesis.cpp:255-286), optional random phase seed.
 int ref_synthesize_pointwise_oracle(const double* object, int n, double wl, double pitch,
-                                    double z, int workers, double* out, std::uint64_t* ops) {
+                                    double z, int workers, int use_seed, std::uint64_t seed,
+                                    double* out, std::uint64_t* ops) {
   return guard([&] {
     const SceneParams scene = make_scene(wl, pitch, z, n);
     const FringeLut unit = build_block_lut(scene, 1, workers);
     OpCounter counter;
-    complex_out(synthesize_pointwise_oracle(real_in(object, n), scene, counter, unit, workers),
+    std::optional<std::uint64_t> s;
+    if (use_seed) s = seed;
+    complex_out(synthesize_pointwise_oracle(real_in(object, n), scene, counter, unit, workers, s),
                 out);
     *ops = counter.get(OpLevel::kPointwiseOracle);
   });

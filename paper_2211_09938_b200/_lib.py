@@ -14,7 +14,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "libwcgh.so"
 
 WCGH_OK, WCGH_EVALIDATION, WCGH_ERUNTIME = 0, 1, 2
-U8, F32, F64 = 0, 1, 2
+U8, F32, F64, C128 = 0, 1, 2, 3
 METHOD_DIRECT, METHOD_LUT, METHOD_FFT = 0, 1, 2
 PHASE_FIXED, PHASE_FP64 = 0, 1
 OP_LEVELS = 5
@@ -92,6 +92,9 @@ _SIGS = [
     ("wcgh_ipc_free_plane", C.c_int, [_VP]),
     ("wcgh_job_download_a_eff", C.c_int, [_VP, _VP]),
     ("wcgh_job_download_points", C.c_int, [_VP, _VP, C.c_int64, C.POINTER(C.c_int64)]),
+    ("wcgh_job_download_a_eff_im", C.c_int, [_VP, _VP]),
+    ("wcgh_job_download_points_im", C.c_int, [_VP, _VP, C.c_int64]),
+    ("wcgh_random_phase_field", C.c_int, [_VP, C.c_int, C.c_int, C.c_uint64, _VP]),
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),
     ("wcgh_job_plane_dev", _VP, [_VP]),
     ("wcgh_job_stats", C.c_int, [_VP, C.POINTER(Stats)]),

@@ -3,6 +3,9 @@
 // entry points. Jobs and multi-GPU are in wcgh_job.cu, file I/O in
 // wcgh_io.cu. Validation mirrors the reference's ValidationError sites; CUDA
 // failures map to WCGH_ERUNTIME.
+#include <complex>
+#include <random>
+
 #include "wcgh_state.cuh"
 
 using namespace wcgh;
@@ -13,6 +16,25 @@ thread_local std::string wcgh::abi::t_last_error;
 extern "C" {
 
 int wcgh_abi_version(void) { return WCGH_ABI_VERSION; }
+
+// The reference's random initial phase, on the host with the same standard
+// library engine and distribution, so the complex object is bit-identical.
+int wcgh_random_phase_field(const double* amplitude, int width, int height, uint64_t seed,
+                            double* out) {
+  return guard(nullptr, [&] {
+    require(amplitude && out, "random_phase_field: NULL argument");
+    require(width >= 0 && height >= 0, "random_phase_field: negative size");
+    std::mt19937_64 rng(seed);
+    // 2 * std::numbers::pi (the same double)
+    std::uniform_real_distribution<double> angle(0.0, 2.0 * 3.141592653589793238462643383279502884);
+    const size_t count = size_t(width) * size_t(height);
+    for (size_t i = 0; i < count; ++i) {
+      const std::complex<double> v = std::polar(amplitude[i], angle(rng));
+      out[2 * i] = v.real();
+      out[2 * i + 1] = v.imag();
+    }
+  });
+}
 
 const char* wcgh_last_error(const wcgh_ctx*) { return t_last_error.c_str(); }
 
@@ -179,6 +201,8 @@ int wcgh_analyze(wcgh_ctx* ctx, const void* object, int obj_dtype, double obj_sc
     require(ctx && object && saliency && plan && out, "analyze: NULL argument");
     validate_plan(*plan);
     require(n >= 8 && n % 8 == 0, "analyze: side must be a positive multiple of 8");
+    require(obj_dtype != WCGH_C128 && sal_dtype != WCGH_C128,
+            "analyze: real images only (complex objects go through a job)");
     std::lock_guard<std::mutex> lk(ctx->mu);
     use_device(ctx);
     cudaStream_t s = ctx->stream;

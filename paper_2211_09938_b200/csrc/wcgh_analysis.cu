@@ -43,6 +43,15 @@ template <>
 __device__ __forceinline__ double load_obj<double>(const double* p, size_t i, double scale) {
   return p[i] * scale;
 }
+// One part of an interleaved complex<double> object (WCGH_C128): the pointer
+// is the first real (or, offset by 8 bytes, imaginary) part; stride 16 bytes.
+struct CPart {
+  double v, other;
+};
+template <>
+__device__ __forceinline__ double load_obj<CPart>(const CPart* p, size_t i, double scale) {
+  return p[i].v * scale;
+}
 
 // Saliency to double: u8 is v * (1/255) like scale_to_unit (image_io.cpp:177-190).
 template <typename T>
@@ -377,10 +386,13 @@ __global__ void __launch_bounds__(1024) k_scan_add(int* __restrict__ offsets, in
 // records are assembled in shared memory and written as one contiguous,
 // coalesced run of 16-byte stores.
 __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict__ a_eff,
+                                                        const float* __restrict__ a_im,
                                                         const int* __restrict__ offsets, int n,
                                                         int n_layers, int off, int layer0,
-                                                        wcgh_point* __restrict__ points) {
+                                                        wcgh_point* __restrict__ points,
+                                                        float* __restrict__ p_im) {
   __shared__ int4 stage[8][128];
+  __shared__ float stage_im[8][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int segs = seg_per_row(n);
   const long long gw = (long long)blockIdx.x * 8 + warp;
@@ -400,9 +412,15 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = (x0 + k < n) ? src[x0 + k] : 0.0f;
   }
+  float w[4] = {0.f, 0.f, 0.f, 0.f};  // imaginary parts (complex objects)
+  if (a_im) {
+    const float* srci = a_im + (size_t(layer) * n + row) * n;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = (x0 + k < n) ? srci[x0 + k] : 0.0f;
+  }
   int nz = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) nz += v[k] != 0.0f;
+  for (int k = 0; k < 4; ++k) nz += v[k] != 0.0f || w[k] != 0.0f;
   int incl = nz;
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(kFull, incl, o);
@@ -413,11 +431,16 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
   const int py = row + off, pl = layer0 + layer;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (v[k] != 0.0f) stage[warp][pos++] = make_int4(x0 + k + off, py, __float_as_int(v[k]), pl);
+    if (v[k] != 0.0f || w[k] != 0.0f) {
+      stage_im[warp][pos] = w[k];
+      stage[warp][pos++] = make_int4(x0 + k + off, py, __float_as_int(v[k]), pl);
+    }
   }
   __syncwarp();
   int4* dst = reinterpret_cast<int4*>(points) + offsets[gw];
   for (int i = lane; i < seg_total; i += 32) dst[i] = stage[warp][i];
+  if (p_im)
+    for (int i = lane; i < seg_total; i += 32) p_im[offsets[gw] + i] = stage_im[warp][i];
 }
 
 // Stage contribution images for the snapshots of the direct and FFT
@@ -444,9 +467,10 @@ __global__ void k_stage_delta(const float* __restrict__ w_stage, int n, int n_la
   out[i] = v;
 }
 
-// Nonzero count per (layer, row, 128-pixel segment) of an fp32 image.
-__global__ void k_seg_counts_f32(const float* __restrict__ img, int n, int n_layers,
-                                 int* __restrict__ counts) {
+// Nonzero count per (layer, row, 128-pixel segment) of an fp32 image (with
+// `img_im`: of the complex image img + i img_im, either part nonzero).
+__global__ void k_seg_counts_f32(const float* __restrict__ img, const float* __restrict__ img_im,
+                                 int n, int n_layers, int* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int segs = seg_per_row(n);
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -454,10 +478,11 @@ __global__ void k_seg_counts_f32(const float* __restrict__ img, int n, int n_lay
   const int seg = int(gw % segs);
   const long long lr = gw / segs;
   const float* row = img + size_t(lr) * n;
+  const float* row_im = img_im ? img_im + size_t(lr) * n : nullptr;
   int nz = 0;
   for (int k = 0; k < 4; ++k) {
     const int x = seg * 128 + 4 * lane + k;
-    nz += (x < n) && row[x] != 0.0f;
+    nz += (x < n) && (row[x] != 0.0f || (row_im && row_im[x] != 0.0f));
   }
   for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(kFull, nz, o);
   if (lane == 0) counts[gw] = nz;
@@ -811,7 +836,8 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
     case WCGH_U8: dispatch_sal<uint8_t>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
     case WCGH_F32: dispatch_sal<float>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
     case WCGH_F64: dispatch_sal<double>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
-    default: throw ValidationError("object dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
+    case WCGH_C128: dispatch_sal<CPart>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;
+    default: throw ValidationError("object dtype must be WCGH_U8, WCGH_F32, WCGH_F64 or WCGH_C128");
   }
   WCGH_CHECK_LAUNCH();
   return 1;
@@ -837,10 +863,11 @@ int launch_scan(const int* counts, int* offsets, int count, cudaStream_t s, DevB
 }
 
 int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers, int off,
-                          int layer0, wcgh_point* points, cudaStream_t s) {
+                          int layer0, wcgh_point* points, cudaStream_t s, const float* a_im,
+                          float* p_im) {
   const long long warps = (long long)n_layers * n * seg_per_row(n);
-  k_compact_points<<<unsigned((warps + 7) / 8), 256, 0, s>>>(a_eff, offsets, n, n_layers, off,
-                                                             layer0, points);
+  k_compact_points<<<unsigned((warps + 7) / 8), 256, 0, s>>>(a_eff, a_im, offsets, n, n_layers,
+                                                             off, layer0, points, p_im);
   WCGH_CHECK_LAUNCH();
   return 1;
 }
@@ -915,9 +942,10 @@ int launch_stage_delta(const float* w_stage, int n, int n_layers, int stage, flo
   return 1;
 }
 
-int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t s) {
+int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t s,
+                          const float* img_im) {
   const long long warps = (long long)n_layers * n * seg_per_row(n);
-  k_seg_counts_f32<<<unsigned((warps + 7) / 8), 256, 0, s>>>(img, n, n_layers, counts);
+  k_seg_counts_f32<<<unsigned((warps + 7) / 8), 256, 0, s>>>(img, img_im, n, n_layers, counts);
   WCGH_CHECK_LAUNCH();
   return 1;
 }

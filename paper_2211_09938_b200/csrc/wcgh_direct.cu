@@ -47,6 +47,24 @@ __device__ __forceinline__ float i2f_small(int v) {
   return __int_as_float(v + 0x4B400000) - 12582912.0f;
 }
 
+// Point record as staged in shared memory: (x, y, amplitude bits, phase
+// offset). A complex amplitude a = |a| e^{i psi} (random-initial-phase
+// objects) becomes |a| and psi as a 0.32 fixed-point fraction of a cycle,
+// added to the point's phase: the per-pixel work is the real-amplitude
+// loop. Real points carry psi = 0 (the record's layer field is not needed).
+__device__ __forceinline__ int4 stage_point(const int4* pts, const float* pim, long long i) {
+  int4 p = pts[i];
+  p.w = 0;
+  if (pim) {
+    const double ar = double(__int_as_float(p.z)), ai = double(pim[i]);
+    double cyc = atan2(ai, ar) * 0.15915494309189533577;  // [-1/2, 1/2]
+    if (cyc < 0.0) cyc += 1.0;
+    p.z = __float_as_int(float(sqrt(ar * ar + ai * ai)));
+    p.w = int(uint32_t(uint64_t(cyc * 4294967296.0 + 0.5)));
+  }
+  return p;
+}
+
 // Chunk c of the point list, restricted to layer l: [s0, s1).
 __device__ __forceinline__ void layer_span(const long long* lb, int l, long long p0, long long p1,
                                            long long& s0, long long& s1) {
@@ -58,8 +76,8 @@ __device__ __forceinline__ void layer_span(const long long* lb, int l, long long
 // the (1+u)^(-1/2) polynomial.
 template <int P, int NC, int AMP, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k_direct_fixed(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
-                   int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
+    k_direct_fixed(const int4* __restrict__ pts, const float* __restrict__ pim,
+                   const long long* __restrict__ layer_begin, int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                    int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
   const int lane = threadIdx.x & 31;
@@ -92,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
+      if (threadIdx.x < nb) sp[threadIdx.x] = stage_point(pts, pim, b + threadIdx.x);
       __syncthreads();
 
 #pragma unroll 1
@@ -102,8 +120,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int dy = y - q.y;
         const int s = dx0 * dx0 + dy * dy;  // exact: |dx|,|dy| < 2^15
         const int s_1 = s + 64 * dx0 + 1024;  // pixel i = 1 (x + 32)
-        uint32_t t = uint32_t(s) * a_hi + __umulhi(uint32_t(s), a_lo) + phi0;
-        const uint32_t t1 = uint32_t(s_1) * a_hi + __umulhi(uint32_t(s_1), a_lo) + phi0;
+        const uint32_t ph0 = phi0 + uint32_t(q.w);  // + the point's phase offset
+        uint32_t t = uint32_t(s) * a_hi + __umulhi(uint32_t(s), a_lo) + ph0;
+        const uint32_t t1 = uint32_t(s_1) * a_hi + __umulhi(uint32_t(s_1), a_lo) + ph0;
         uint32_t D = t1 - t;
         const float fdx = i2f_small(dx0), fdy = i2f_small(dy);
         float u = fmaf(fdx * c, fdx, fdy * fdy * c);
@@ -157,8 +176,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // fp32 sin/cos. Accuracy mode (FP64-pipe bound).
 template <int P>
 __global__ void __launch_bounds__(kThreads)
-    k_direct_fp64(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
-                  int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
+    k_direct_fp64(const int4* __restrict__ pts, const float* __restrict__ pim,
+                  const long long* __restrict__ layer_begin, int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                   int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
   const int lane = threadIdx.x & 31;
@@ -185,18 +204,19 @@ __global__ void __launch_bounds__(kThreads)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
+      if (threadIdx.x < nb) sp[threadIdx.x] = stage_point(pts, pim, b + threadIdx.x);
       __syncthreads();
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
         const int4 q = sp[j];
         const double ddy = double(y - q.y) * pitch;
         const double a = double(__int_as_float(q.z));
+        const double psi = double(uint32_t(q.w)) * (two_pi / 4294967296.0);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
           const double ddx = double(xb + 32 * i - q.x) * pitch;
           const double r = sqrt(ddx * ddx + ddy * ddy + z2);
-          const double kr = k * r;
+          const double kr = fma(k, r, psi);
           const double red = kr - two_pi * rint(kr * (1.0 / two_pi));
           const float am = float(a / r);
           float sn, cs;
@@ -255,6 +275,7 @@ struct LaunchArgs {
   dim3 grid;
   cudaStream_t s;
   const int4* pts;
+  const float* pim;
   const long long* lb;
   int L;
   long long np;
@@ -267,7 +288,7 @@ template <int P, int NC, int AMP>
 void launch_fixed(const LaunchArgs& a) {
   constexpr int MINB = 2;
   k_direct_fixed<P, NC, AMP, MINB><<<a.grid, kThreads, 0, a.s>>>(
-      a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+      a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
 }
 
 template <int P, int NC>
@@ -372,7 +393,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
                   cudaStream_t stream, DirectTiming* timing, double* updates_out,
-                  const PeerPlanes* peers) {
+                  const PeerPlanes* peers, const float* pim_dev) {
   require(n_layers >= 1 && n_layers <= kMaxLayers, "direct: 1..16 layers");
   require(rows >= 1 && row0 >= 0 && row0 + rows <= nh, "direct: row band outside the plane");
   require(phase_mode == WCGH_PHASE_FIXED || phase_mode == WCGH_PHASE_FP64,
@@ -409,16 +430,16 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
     const int ng = std::min(group, n_chunks - g0);
     LaunchArgs a{dim3(unsigned(tiles_x * tiles_y), unsigned(ng)), stream,
-                 reinterpret_cast<const int4*>(pts_dev), lb_dev, n_layers, n_points, g0, nh,
+                 reinterpret_cast<const int4*>(pts_dev), pim_dev, lb_dev, n_layers, n_points, g0, nh,
                  row0, rows, tiles_x, partial, band};
     if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), stream));
     if (phase_mode == WCGH_PHASE_FP64) {
       if (P == 32)
-        k_direct_fp64<32><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<32><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
       else if (P == 16)
-        k_direct_fp64<16><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<16><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
       else
-        k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
     } else {
       if (P == 32)
         launch_fixed_nc<32>(plan, a);

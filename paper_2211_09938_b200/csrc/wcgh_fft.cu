@@ -48,13 +48,14 @@ __global__ void k_fringe_grid(double wavelength, double pitch, double z, int nh,
   g[i] = make_float2(float(c / r), float(s / r));
 }
 
-// A_eff (No x No fp32, one layer) -> real part of the L x L grid at (off+y, off+x).
-__global__ void k_scatter(const float* __restrict__ a, int no, int off, int L,
-                          float2* __restrict__ grid) {
+// A_eff (No x No fp32, one layer; a_im: imaginary part or NULL) -> the L x L
+// grid at (off+y, off+x).
+__global__ void k_scatter(const float* __restrict__ a, const float* __restrict__ a_im, int no,
+                          int off, int L, float2* __restrict__ grid) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= size_t(no) * no) return;
   const int x = int(i % no), y = int(i / no);
-  grid[size_t(off + y) * L + off + x] = make_float2(a[i], 0.f);
+  grid[size_t(off + y) * L + off + x] = make_float2(a[i], a_im ? a_im[i] : 0.f);
 }
 
 // acc (+)= fa * ff (complex), elementwise.
@@ -123,7 +124,7 @@ void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cu
 
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
                          int rows, float2* out, cudaStream_t s, DirectTiming* timing,
-                         const PeerPlanes* peers) {
+                         const PeerPlanes* peers, const float* a_im) {
   const int L = fp.L;
   const size_t L2 = size_t(L) * L;
   WCGH_CUFFT(cufftSetStream(fp.plan, s));
@@ -133,7 +134,8 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
   if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), s));
   for (int l = 0; l < fp.n_layers; ++l) {
     WCGH_CUDA(cudaMemsetAsync(grid, 0, sizeof(float2) * L2, s));
-    k_scatter<<<blocks_for(size_t(no) * no), 256, 0, s>>>(a_eff + size_t(no) * no * l, no, off, L, grid);
+    k_scatter<<<blocks_for(size_t(no) * no), 256, 0, s>>>(
+        a_eff + size_t(no) * no * l, a_im ? a_im + size_t(no) * no * l : nullptr, no, off, L, grid);
     WCGH_CHECK_LAUNCH();
     dbg(s, "scatter");
     WCGH_CUFFT(cufftExecC2C(fp.plan, reinterpret_cast<cufftComplex*>(grid),

@@ -150,7 +150,8 @@ DirectLayer make_direct_layer(const wcgh_layer& L);
 // Launches K3 (and the chunk reductions) on `stream`. pts: device, sorted by
 // layer; layer_begin: host array (n_layers + 1). out: device rows x nh
 // complex64. Returns the number of kernel launches; if `timing` is given,
-// brackets every K3 launch with an event pair.
+// brackets every K3 launch with an event pair. pim (device, optional): the
+// points' imaginary amplitudes (complex objects; pts[i].a is the real part).
 struct DirectScratch {
   DevBuf partial;
 };
@@ -158,7 +159,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
                   double max_dx, double max_dy, float2* out_dev, DirectScratch& scratch,
                   cudaStream_t stream, DirectTiming* timing, double* updates_out,
-                  const PeerPlanes* peers = nullptr);
+                  const PeerPlanes* peers = nullptr, const float* pim = nullptr);
 
 // ---- analysis (K1 + K2) ----------------------------------------------------
 
@@ -195,6 +196,8 @@ __host__ __device__ inline int seg_per_row(int n) { return (n + 127) / 128; }
 // Error flag bits written by the analysis kernel.
 enum : int { kErrObjectNonFinite = 1, kErrSaliencyRange = 2 };
 
+// WCGH_C128: analyses one part of the complex object; `obj` points at the
+// first real part (or, 8 bytes on, the first imaginary part).
 int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void* sal,
                     int sal_dtype, int n, int n_layers, const wcgh_plan& plan,
                     const AnalysisOut& out, cudaStream_t stream);
@@ -204,14 +207,18 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
 int launch_scan(const int* counts, int* offsets, int count, cudaStream_t stream,
                 DevBuf* scratch = nullptr);
 // Ordered compaction of nonzero A_eff into points (hologram coordinates).
+// With a_im (complex objects): kept where either part is nonzero, imaginary
+// parts written to p_im in point order.
 int launch_compact_points(const float* a_eff, const int* offsets, int n, int n_layers,
-                          int offset, int layer0, wcgh_point* points, cudaStream_t stream);
+                          int offset, int layer0, wcgh_point* points, cudaStream_t stream,
+                          const float* a_im = nullptr, float* p_im = nullptr);
 // Ordered compaction of nonzero mask bytes into cell indices y*m+x.
 int launch_mask_counts(const uint8_t* mask, int m, int* seg_counts, cudaStream_t stream);
 // Stage s's amplitude contribution image (snapshots of the direct/FFT methods).
 int launch_stage_delta(const float* w_stage, int n, int n_layers, int stage, float* out,
                        cudaStream_t stream);
-int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t stream);
+int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cudaStream_t stream,
+                          const float* img_im = nullptr);
 int launch_compact_mask(const uint8_t* mask, int m, const int* offsets, uint32_t* cells,
                         cudaStream_t stream);
 
@@ -241,10 +248,11 @@ struct FftPlan {
 };
 // Per-layer fringe spectra on the 2Nh x 2Nh grid (precompute).
 void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cudaStream_t stream);
-// out (rows x nh) = band of sum_layers A_eff_l (*) F_l.
+// out (rows x nh) = band of sum_layers A_eff_l (*) F_l; a_im (optional): the
+// imaginary part of a complex A_eff.
 int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int nh, int row0,
                          int rows, float2* out, cudaStream_t stream, DirectTiming* timing,
-                         const PeerPlanes* peers = nullptr);
+                         const PeerPlanes* peers = nullptr, const float* a_im = nullptr);
 
 // ---- reconstruction and SSIM (K6, K7) --------------
 struct ReconPlan {
@@ -308,9 +316,11 @@ int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t strea
 void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t stream);
 // out (rows x nh complex64, overwritten) = superposition of the stage's
 // listed cells with the block-B LUT; object grid offset `off` on the plane.
+// accumulate: out += instead; rotate: out += i * superposition (the
+// imaginary weights of a complex object, by linearity).
 int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
                      int rows, float2* out, DevBuf& partial, cudaStream_t stream,
-                     DirectTiming* timing, bool accumulate);
+                     DirectTiming* timing, bool accumulate, bool rotate = false);
 // Dense weight grid convenience: builds the list, reads nnz (synchronizes),
 // superposes.
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,

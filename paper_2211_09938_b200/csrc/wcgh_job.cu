@@ -32,6 +32,7 @@ void wcgh::abi::job_validate(const wcgh_desc& d) {
           "job: unknown phase mode");
   dtype_size(d.obj_dtype);
   dtype_size(d.sal_dtype);
+  require(d.sal_dtype != WCGH_C128, "saliency dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
   if (d.method == WCGH_METHOD_LUT) {
     for (int l = 1; l < d.n_layers; ++l)
       require(d.layers[l].wavelength == d.layers[0].wavelength && d.layers[l].pitch == d.layers[0].pitch,
@@ -71,7 +72,7 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     WCGH_CUDA(cudaMallocHost(&j->h_offsets, sizeof(int64_t) * (L + 1)));
     WCGH_CUDA(cudaMallocHost(&j->h_ops, sizeof(unsigned long long) * WCGH_OP_LEVELS * L));
     WCGH_CUDA(cudaMallocHost(&j->h_err, sizeof(int) * 4));
-    WCGH_CUDA(cudaMallocHost(&j->h_tot, sizeof(int) * 3 * 4 * kMaxLayers));
+    WCGH_CUDA(cudaMallocHost(&j->h_tot, sizeof(int) * 2 * 3 * 4 * kMaxLayers));
     for (auto& e : j->ev) WCGH_CUDA(cudaEventCreate(&e));
     if (d.method == WCGH_METHOD_DIRECT) {
       j->points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1));
@@ -139,18 +140,39 @@ int wcgh_job_upload_dev(wcgh_job* job, const void* object, const void* saliency)
 
 namespace {
 
+// K1 (+ the compaction counts of the direct/FFT methods). A complex object
+// (random initial phase, synthesis.cpp:205-219) is analysed part by part,
+// as the reference does (pyr_re, pyr_im): the gates depend on the saliency
+// only, so the two passes gate identically and the operator counts are the
+// first pass's.
 void run_analysis(wcgh_job* j, cudaStream_t s, bool lut) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
-  WCGH_CUDA(cudaMemsetAsync(j->ops.p, 0, sizeof(unsigned long long) * WCGH_OP_LEVELS * L + sizeof(int), s));
+  const bool cplx = j->complex_obj();
+  const size_t ops_bytes = sizeof(unsigned long long) * WCGH_OP_LEVELS * L;
+  WCGH_CUDA(cudaMemsetAsync(j->ops.p, 0, ops_bytes + sizeof(int), s));
   AnalysisOut ao;
   ao.a_eff = j->a_eff.as<float>();
-  ao.seg_counts = lut ? nullptr : j->seg_counts.as<int>();
+  ao.seg_counts = (lut || cplx) ? nullptr : j->seg_counts.as<int>();
   ao.w_stage = lut ? j->w_stage.as<float>() : nullptr;
   ao.ops = j->ops.as<unsigned long long>();
   ao.err = reinterpret_cast<int*>(ao.ops + WCGH_OP_LEVELS * L);
   launch_analysis(j->obj.p, d.obj_dtype, d.obj_scale, j->sal.p, d.sal_dtype, No, L, d.plan, ao, s);
   j->stats.total_launches += 1;
+  if (!cplx) return;
+  AnalysisOut bo = ao;
+  bo.a_eff = static_cast<float*>(j->a_eff_im.reserve(sizeof(float) * j->in_elems * L));
+  bo.w_stage = lut ? static_cast<float*>(j->w_stage_im.reserve(sizeof(float) * wstage_len(No) * L))
+                   : nullptr;
+  bo.ops = static_cast<unsigned long long*>(j->ops_im.reserve(ops_bytes));
+  WCGH_CUDA(cudaMemsetAsync(bo.ops, 0, ops_bytes, s));
+  launch_analysis(static_cast<const char*>(j->obj.p) + sizeof(double), d.obj_dtype, d.obj_scale,
+                  j->sal.p, d.sal_dtype, No, L, d.plan, bo, s);
+  j->stats.total_launches += 1;
+  if (!lut) {
+    launch_seg_counts_f32(ao.a_eff, No, L, j->seg_counts.as<int>(), s, bo.a_eff);
+    j->stats.total_launches += 1;
+  }
 }
 
 void finish_stats(wcgh_job* j, const unsigned long long* ops) {
@@ -173,9 +195,13 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
   const bool fft = d.method == WCGH_METHOD_FFT;
   const int scan_launches = launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s,
                                         &j->scan_scratch);
+  const bool cplx = j->complex_obj();
+  const float* a_im = cplx ? j->a_eff_im.as<float>() : nullptr;
+  float* p_im = cplx && !fft ? static_cast<float*>(j->points_im.reserve(sizeof(float) * (j->in_elems * L + 1)))
+                             : nullptr;
   if (!fft)
     launch_compact_points(j->a_eff.as<float>(), j->seg_offsets.as<int>(), No, L, j->off, 0,
-                          j->points.as<wcgh_point>(), s);
+                          j->points.as<wcgh_point>(), s, a_im, p_im);
   j->stats.total_launches += scan_launches + (fft ? 0 : 1);
   WCGH_CUDA(cudaEventRecord(j->ev[1], s));
   // layer boundaries of the compacted list, ops and validation flags
@@ -208,11 +234,11 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
     j->stats.updates = double(lb[L]) * double(d.rows) * double(d.plane_size);
     launches = launch_fft_synthesis(j->fft, j->a_eff.as<float>(), No, j->off, d.plane_size,
                                     d.row0, d.rows, j->plane.as<float2>(), s, &j->timing,
-                                    &j->peers);
+                                    &j->peers, a_im);
   } else {
     launches = launch_direct(j->points.as<wcgh_point>(), lb, L, d.layers, d.plane_size, d.row0,
                              d.rows, d.phase_mode, far, max_dy, j->plane.as<float2>(), j->direct,
-                             s, &j->timing, &j->stats.updates, &j->peers);
+                             s, &j->timing, &j->stats.updates, &j->peers, p_im);
   }
   j->stats.synth_launches = j->timing.launches();
   j->stats.total_launches += launches;
@@ -251,14 +277,24 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
   size_t wofs[4];
   wofs[0] = 0;
   for (int st = 1; st < 4; ++st) wofs[st] = wofs[st - 1] + size_t(ms[st - 1]) * ms[st - 1];
-  // run lists of the nonzero gated cells per (layer, stage) (K2 for the LUT path)
+  // run lists of the nonzero gated cells per (layer, stage) (K2 for the LUT
+  // path); a complex object adds the lists of its imaginary weights
+  const bool cplx = j->complex_obj();
   while (j->cells.size() < size_t(L) * 4) j->cells.push_back(std::make_unique<StageCells>());
+  while (cplx && j->cells_im.size() < size_t(L) * 4) j->cells_im.push_back(std::make_unique<StageCells>());
+  int* h_tot_im = j->h_tot + 3 * 4 * kMaxLayers;
   for (int l = 0; l < L; ++l)
     for (int st = 0; st < 4; ++st) {
       const float* w = j->w_stage.as<float>() + wstage_len(No) * l + wofs[st];
       StageCells& sc = *j->cells[size_t(l) * 4 + st];
       j->stats.total_launches += launch_stage_cells(w, ms[st], sc, s);
       stage_cells_totals_async(sc, j->h_tot + 3 * (l * 4 + st), s);
+      if (cplx) {
+        const float* wi = j->w_stage_im.as<float>() + wstage_len(No) * l + wofs[st];
+        StageCells& si = *j->cells_im[size_t(l) * 4 + st];
+        j->stats.total_launches += launch_stage_cells(wi, ms[st], si, s);
+        stage_cells_totals_async(si, h_tot_im + 3 * (l * 4 + st), s);
+      }
     }
   WCGH_CUDA(cudaMemcpyAsync(j->h_ops, j->ops.p, sizeof(unsigned long long) * WCGH_OP_LEVELS * L, cudaMemcpyDeviceToHost, s));
   WCGH_CUDA(cudaMemcpyAsync(j->h_err, j->ops.as<unsigned long long>() + WCGH_OP_LEVELS * L, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -268,7 +304,7 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
   finish_stats(j, j->h_ops);
   if (!synth) {  // front end only (wcgh_job_analyze): nonzero gated cells
     long long cells = 0;
-    for (int k = 0; k < 4 * L; ++k) cells += j->h_tot[3 * k + 2];
+    for (int k = 0; k < 4 * L; ++k) cells += j->h_tot[3 * k + 2] + (cplx ? h_tot_im[3 * k + 2] : 0);
     j->stats.n_points = cells;
     WCGH_CUDA(cudaEventElapsedTime(&j->stats.ms_analysis, j->ev[0], j->ev[1]));
     j->stats.ms_total = j->stats.ms_analysis;
@@ -289,6 +325,16 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
                                                   j->off, d.row0, d.rows, sp + band * st,
                                                   j->lut_partial, s, &j->timing, l > 0);
       cells += sc.nnz;
+      if (cplx) {  // + i * (imaginary weights' superposition), by linearity
+        StageCells& si = *j->cells_im[k];
+        si.n_runs = h_tot_im[3 * k];
+        si.n_dense = h_tot_im[3 * k + 1];
+        si.nnz = h_tot_im[3 * k + 2];
+        j->stats.total_launches += launch_lut_stage(j->lut_base[k], d.plane_size, blocks[st], si,
+                                                    j->off, d.row0, d.rows, sp + band * st,
+                                                    j->lut_partial, s, &j->timing, true, true);
+        cells += si.nnz;
+      }
     }
   j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));
@@ -328,17 +374,23 @@ void compute_stage_planes(wcgh_job* j, cudaStream_t s) {
   const double far = double(j->off + No - 1);
   const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
                                  std::fabs(double(d.row0 + d.rows - 1) - j->off));
+  const bool cplx = j->complex_obj();
+  float* img_im = cplx ? static_cast<float*>(j->snap_img_im.reserve(sizeof(float) * j->in_elems * L)) : nullptr;
+  float* pim = cplx ? static_cast<float*>(j->snap_points_im.reserve(sizeof(float) * (j->in_elems * L + 1)))
+                    : nullptr;
   for (int st = 0; st < 4; ++st) {
     launch_stage_delta(j->w_stage.as<float>(), No, L, st, img, s);
+    if (cplx) launch_stage_delta(j->w_stage_im.as<float>(), No, L, st, img_im, s);
     float2* out = planes + band * st;
     if (d.method == WCGH_METHOD_FFT) {
-      launch_fft_synthesis(j->fft, img, No, j->off, d.plane_size, d.row0, d.rows, out, s, nullptr);
+      launch_fft_synthesis(j->fft, img, No, j->off, d.plane_size, d.row0, d.rows, out, s, nullptr,
+                           nullptr, img_im);
       continue;
     }
-    launch_seg_counts_f32(img, No, L, j->seg_counts.as<int>(), s);
+    launch_seg_counts_f32(img, No, L, j->seg_counts.as<int>(), s, img_im);
     launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s, &j->scan_scratch);
     wcgh_point* pts = static_cast<wcgh_point*>(j->snap_points.reserve(sizeof(wcgh_point) * (j->in_elems * L + 1)));
-    launch_compact_points(img, j->seg_offsets.as<int>(), No, L, j->off, 0, pts, s);
+    launch_compact_points(img, j->seg_offsets.as<int>(), No, L, j->off, 0, pts, s, img_im, pim);
     for (int l = 0; l <= L; ++l)
       WCGH_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(j->h_offsets) + l,
                                 j->seg_offsets.as<int>() + per_layer * size_t(l), sizeof(int),
@@ -347,7 +399,7 @@ void compute_stage_planes(wcgh_job* j, cudaStream_t s) {
     int64_t lb[kMaxLayers + 1];
     for (int l = 0; l <= L; ++l) lb[l] = reinterpret_cast<const int*>(j->h_offsets)[l];
     launch_direct(pts, lb, L, d.layers, d.plane_size, d.row0, d.rows, d.phase_mode, far, max_dy,
-                  out, j->direct, s, nullptr, nullptr);
+                  out, j->direct, s, nullptr, nullptr, nullptr, pim);
   }
   sync(s);
   j->stats = keep;
@@ -476,6 +528,35 @@ int wcgh_job_download_points(wcgh_job* job, wcgh_point* out, int64_t capacity, i
     use_device(job->ctx);
     cudaStream_t s = job->ctx->stream;
     WCGH_CUDA(cudaMemcpyAsync(out, job->points.p, sizeof(wcgh_point) * size_t(n), cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_job_download_a_eff_im(wcgh_job* job, float* out) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && out, "job_download_a_eff_im: NULL argument");
+    require(job->complex_obj(), "job_download_a_eff_im: the job's object is real (not WCGH_C128)");
+    require(job->a_eff_im.p != nullptr, "job_download_a_eff_im: run or analyze the job first");
+    use_device(job->ctx);
+    cudaStream_t s = job->ctx->stream;
+    WCGH_CUDA(cudaMemcpyAsync(out, job->a_eff_im.p, sizeof(float) * job->in_elems * job->desc.n_layers,
+                              cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+int wcgh_job_download_points_im(wcgh_job* job, float* out, int64_t capacity) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && out, "job_download_points_im: NULL argument");
+    require(job->complex_obj(), "job_download_points_im: the job's object is real (not WCGH_C128)");
+    require(job->desc.method == WCGH_METHOD_DIRECT,
+            "job_download_points: the compacted point list is built by the direct method");
+    require(job->points_im.p != nullptr, "job_download_points_im: run or analyze the job first");
+    const int64_t n = int64_t(job->stats.n_points);
+    require(capacity >= n, "job_download_points_im: capacity below the point count");
+    use_device(job->ctx);
+    cudaStream_t s = job->ctx->stream;
+    WCGH_CUDA(cudaMemcpyAsync(out, job->points_im.p, sizeof(float) * size_t(n), cudaMemcpyDeviceToHost, s));
     sync(s);
   });
 }

@@ -277,12 +277,22 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
   }
 }
 
-// out (+)= sum of `n` partial planes in order, fp64 accumulation.
+// out (+)= sum of `n` partial planes in order, fp64 accumulation. rotate:
+// out += i * sum (imaginary LUT weights of a complex object).
 __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, size_t count,
-                                  int accumulate, float2* __restrict__ out) {
+                                  int accumulate, int rotate, float2* __restrict__ out) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double re = 0.0, im = 0.0;
+  if (rotate) {
+    for (int c = 0; c < n; ++c) {
+      const float2 v = partial[size_t(c) * count + i];
+      re += v.x;
+      im += v.y;
+    }
+    out[i] = make_float2(float(double(out[i].x) - im), float(double(out[i].y) + re));
+    return;
+  }
   if (accumulate) {
     re = out[i].x;
     im = out[i].y;
@@ -403,8 +413,9 @@ void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t s) 
 
 int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
                      int rows, float2* out, DevBuf& partial, cudaStream_t s, DirectTiming* timing,
-                     bool accumulate) {
+                     bool accumulate, bool rotate) {
   const size_t band = size_t(rows) * nh;
+  require(!rotate || accumulate, "LUT superposition: a rotated stage accumulates");
   if (sc.n_runs == 0) {
     if (!accumulate) WCGH_CUDA(cudaMemsetAsync(out, 0, band * sizeof(float2), s));
     return 0;
@@ -438,7 +449,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
     WCGH_CHECK_LAUNCH();
     if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
     k_reduce_partials<<<unsigned((band + 255) / 256), 256, 0, s>>>(part, ng, band,
-                                                                  accumulate || g0 > 0, out);
+                                                                  accumulate || g0 > 0, rotate, out);
     WCGH_CHECK_LAUNCH();
     launches += 2;
   }

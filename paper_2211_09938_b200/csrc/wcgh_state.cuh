@@ -51,13 +51,17 @@ struct wcgh_job {
   int64_t* h_offsets = nullptr;       // n_layers + 1
   unsigned long long* h_ops = nullptr;  // n_layers * 5
   int* h_err = nullptr;
-  int* h_tot = nullptr;  // LUT: (runs, dense steps, nnz) per stage
+  int* h_tot = nullptr;  // LUT: (runs, dense steps, nnz) per stage (re, then im lists)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   wcgh_stats stats{};
   bool uploaded = false;
   bool ran = false;           // a run finished since the last upload
   bool stages_ready = false;  // stage_planes hold the per-stage planes of the last run
   wcgh::DevBuf snap_img, snap_points;  // direct/FFT snapshots (computed on demand)
+  // complex objects (obj_dtype WCGH_C128): imaginary-part counterparts
+  wcgh::DevBuf a_eff_im, w_stage_im, ops_im, points_im, snap_img_im, snap_points_im;
+  std::vector<std::unique_ptr<wcgh::StageCells>> cells_im;
+  bool complex_obj() const { return desc.obj_dtype == WCGH_C128; }
   wcgh::PeerPlanes peers;              // fused row-tile gather targets (wcgh_job_set_peer_planes)
   ~wcgh_job() {
     if (h_tot) cudaFreeHost(h_tot);
@@ -82,7 +86,8 @@ inline size_t dtype_size(int dt) {
     case WCGH_U8: return 1;
     case WCGH_F32: return 4;
     case WCGH_F64: return 8;
-    default: throw ValidationError("dtype must be WCGH_U8, WCGH_F32 or WCGH_F64");
+    case WCGH_C128: return 16;
+    default: throw ValidationError("dtype must be WCGH_U8, WCGH_F32, WCGH_F64 or WCGH_C128");
   }
 }
 

@@ -28,13 +28,13 @@ class JobSpec:
     phase: str = "fixed"          # "fixed" | "fp64"
     row0: int = 0
     rows: int | None = None
-    obj_dtype: str = "u8"
+    obj_dtype: str = "u8"         # "u8" | "f32" | "f64" | "c128" (complex object)
     obj_scale: float = 1.0
     sal_dtype: str = "u8"
 
 
-_DT = {"u8": L.U8, "f32": L.F32, "f64": L.F64}
-_NP = {"u8": np.uint8, "f32": np.float32, "f64": np.float64}
+_DT = {"u8": L.U8, "f32": L.F32, "f64": L.F64, "c128": L.C128}
+_NP = {"u8": np.uint8, "f32": np.float32, "f64": np.float64, "c128": np.complex128}
 
 
 def _make_desc(spec: JobSpec):
@@ -116,10 +116,22 @@ class HologramJob:
         return out
 
     def download_a_eff(self) -> np.ndarray:
-        """A_eff of the last run/analyze, (n_layers, No, No) fp32."""
+        """A_eff of the last run/analyze, (n_layers, No, No) fp32 (complex64
+        for a "c128" object)."""
         no = self.spec.object_size
         out = np.empty((len(self.spec.layers), no, no), np.float32)
         L.check(self.ctx.lib.wcgh_job_download_a_eff(self.h, L.ptr(out)))
+        if self.spec.obj_dtype != "c128":
+            return out
+        im = np.empty_like(out)
+        L.check(self.ctx.lib.wcgh_job_download_a_eff_im(self.h, L.ptr(im)))
+        return (out + 1j * im).astype(np.complex64)
+
+    def download_points_im(self) -> np.ndarray:
+        """Imaginary amplitudes of download_points()' records ("c128" objects)."""
+        n = self.stats()["n_points"]
+        out = np.empty(n, np.float32)
+        L.check(self.ctx.lib.wcgh_job_download_points_im(self.h, L.ptr(out), n))
         return out
 
     def download_points(self) -> np.ndarray:

@@ -249,6 +249,19 @@ def ssim(a: np.ndarray, b: np.ndarray, window: int = 8, k1: float = 0.01, k2: fl
     return float(out.value)
 
 
+def random_phase_field(amplitude: np.ndarray, seed: int) -> np.ndarray:
+    """random_phase_field (synthesis.cpp:288-296) through the library's host
+    function: polar(amplitude, U[0, 2pi)) from std::mt19937_64(seed) — the
+    reference's own engine, so the complex128 result is bit-identical."""
+    a = np.ascontiguousarray(amplitude, np.float64)
+    if a.ndim != 2:
+        raise L.ValidationError("random_phase_field: amplitude must be 2-D")
+    out = np.empty(a.shape, np.complex128)
+    L.check(L.load().wcgh_random_phase_field(L.ptr(a), a.shape[1], a.shape[0],
+                                             int(seed) & 0xFFFFFFFFFFFFFFFF, L.ptr(out)))
+    return out
+
+
 def write_cghl(path, lut: np.ndarray, n: int, block: int, layer) -> None:
     """lut_cache_store (fringe_lut.cpp:95-115): CGHL header + f32 (re, im) payload."""
     lut = np.ascontiguousarray(lut, np.complex64)

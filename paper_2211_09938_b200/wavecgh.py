@@ -477,12 +477,19 @@ def refine(plane: np.ndarray, detail_h, detail_v, detail_d, saliency_finer, lut:
         mask.on = on
 
 
-def _job(n_obj: int, scene: SceneParams, plan: RefinementPlan, method: str) -> HologramJob:
+def _job(n_obj: int, scene: SceneParams, plan: RefinementPlan, method: str,
+         obj_dtype: str = "f64") -> HologramJob:
     return HologramJob(JobSpec(object_size=n_obj, plane_size=scene.plane_size(),
                                layers=[scene.layer()], t_ll=plan.t_ll, t_l=plan.t_l,
                                t_full=plan.t_full, enable_ll=plan.enable_ll,
                                enable_l=plan.enable_l, enable_full=plan.enable_full,
-                               method=method, obj_dtype="f64", sal_dtype="f64"))
+                               method=method, obj_dtype=obj_dtype, sal_dtype="f64"))
+
+
+def random_phase_field(amplitude: np.ndarray, seed: int) -> np.ndarray:
+    """synthesis.cpp:288-296: polar(amplitude, U[0, 2pi)) from mt19937_64(seed),
+    drawn on the host by the library with the reference's engine (bit-identical)."""
+    return stages.random_phase_field(amplitude, seed)
 
 
 def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: SceneParams,
@@ -507,12 +514,12 @@ def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: Sce
             raise ValidationError(f"synthesize_progressive: missing LUT for block size {b}")
     if not (luts.of(1).scene() == scene):
         raise ValidationError("synthesize_progressive: LUTs built for a different scene")
-    if random_phase_seed is not None:
-        raise ValidationError("synthesize_progressive: random initial phase is not supported "
-                              "by the GPU path")
-    job = _job(n, scene, plan, method)
+    # random initial phase (synthesis.cpp:205-214): a complex object, analysed
+    # and synthesised part by part on the device (WCGH_C128 job)
+    src = obj if random_phase_seed is None else random_phase_field(obj, random_phase_seed)
+    job = _job(n, scene, plan, method, "f64" if random_phase_seed is None else "c128")
     try:
-        job(np.ascontiguousarray(obj), np.ascontiguousarray(sal))
+        job(np.ascontiguousarray(src), np.ascontiguousarray(sal))
         st = job.stats()
         snaps = job.download_stages()
     finally:
@@ -545,12 +552,20 @@ def synthesize_pointwise_oracle(object_: np.ndarray, scene: SceneParams, counter
     if not (unit_lut.scene() == scene):
         raise ValidationError("pointwise oracle: LUT built for a different scene")
     _require_finite(obj, "object")
-    if random_phase_seed is not None:
-        raise ValidationError("pointwise oracle: random initial phase is not supported by the GPU path")
     plane = np.zeros((n, n), np.complex64)
-    ops = stages.apply_blocks(plane, scene.layer(), 1, np.arange(n * n), obj.ravel())
+    cells = np.arange(n * n)
+    if random_phase_seed is None:
+        ops = stages.apply_blocks(plane, scene.layer(), 1, cells, obj.ravel())
+        counter.add(OpLevel.POINTWISE_ORACLE, ops)
+        return plane.astype(np.complex128)
+    # complex amplitudes (synthesis.cpp:269-284): real and imaginary weights
+    # superposed separately, combined by linearity; one operator per cell
+    rotated = random_phase_field(obj, random_phase_seed)
+    ops = stages.apply_blocks(plane, scene.layer(), 1, cells, rotated.real.ravel())
+    plane_im = np.zeros((n, n), np.complex64)
+    stages.apply_blocks(plane_im, scene.layer(), 1, cells, rotated.imag.ravel())
     counter.add(OpLevel.POINTWISE_ORACLE, ops)
-    return plane.astype(np.complex128)
+    return plane.astype(np.complex128) + 1j * plane_im.astype(np.complex128)
 
 
 # ---- fft.hpp / angular_spectrum.hpp / metrics.hpp (validation, on the device) ----

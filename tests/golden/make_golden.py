@@ -140,7 +140,33 @@ def main():
         O.ref_lut_cache_store(path, WL, 8e-6, 0.1, 16, 2)
         save("ref_cghl_n16_b2", cghl_bytes=np.frombuffer(path.read_bytes(), np.uint8),
              lut=O.ref_build_block_lut(WL, 8e-6, 0.1, 16, 2))
+    random_phase()
+
+
+def random_phase():
+    """10. Random initial phase (synthesis.cpp:205-219, 269-296): the rotated
+    object, the four snapshots under the default plan, the telescoping case of
+    test_synthesis.cpp:408-433 (uniform saliency, zero thresholds, vs the
+    direct Eq.(1) sum of the rotated field) and the point-wise oracle."""
+    out = {}
+    for n, seed in ((16, 424242), (32, 77)):
+        obj = O.ref_random_image(n, n, 13 + n)
+        sal = O.ref_random_image(n, n, 14 + n)
+        rot = O.ref_random_phase_field(obj, seed)
+        planes, masks, ops = O.ref_synthesize_progressive(obj, sal, WL, 8e-6, 0.1, seed=seed)
+        tele, _, tops = O.ref_synthesize_progressive(obj, np.ones((n, n)), WL, 8e-6, 0.1,
+                                                     t=(0.0, 0.0, 0.0), seed=seed)
+        pw, pops = O.ref_pointwise_oracle(obj, WL, 8e-6, 0.1, seed=seed)
+        out.update({f"object{n}": obj, f"saliency{n}": sal, f"seed{n}": np.array(seed, np.uint64),
+                    f"rotated{n}": rot, f"planes{n}": planes, f"masks{n}": masks, f"ops{n}": ops,
+                    f"tele{n}": tele[3], f"tele_ops{n}": tops,
+                    f"direct{n}": O.ref_pointwise_hologram_reference(rot, WL, 8e-6, 0.1),
+                    f"pointwise{n}": pw, f"pointwise_ops{n}": np.array(pops, np.uint64)})
+    save("ref_random_phase", **out)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--random-phase"]:
+        random_phase()
+    else:
+        main()

@@ -172,3 +172,25 @@ def test_recon_and_ssim_oracles_match_reference_goldens():
         b = g["ssim_b"][off:off + n * n].reshape(n, n)
         off += n * n
         assert abs(O.ssim(a, b, int(win)) - v) <= 1e-12
+
+
+def test_random_phase_field_and_complex_restatement_pins():
+    """random_phase_field (synthesis.cpp:288-296) through the library's host
+    function — the reference's own engine, no device work — is bit-identical
+    to the reference's; the complex synthesis restated by linearity (pyr_re,
+    pyr_im; synthesis.cpp:205-251) reproduces the reference's snapshots."""
+    from paper_2211_09938_b200 import stages
+    g = golden("ref_random_phase")
+    for n in (16, 32):
+        obj, sal, rot = g[f"object{n}"], g[f"saliency{n}"], g[f"rotated{n}"]
+        assert np.array_equal(stages.random_phase_field(obj, int(g[f"seed{n}"])), rot)
+        assert np.allclose(np.abs(rot), obj, rtol=1e-12, atol=0)  # test_synthesis.cpp:425-431
+        luts = [O.build_block_lut(WL, 8e-6, 0.1, n, b) for b in (1, 2, 4, 8)]
+        pr, masks, ops = O.synthesize_progressive(rot.real, sal, WL, 8e-6, 0.1, luts=luts)
+        pi, masks_i, _ = O.synthesize_progressive(rot.imag, sal, WL, 8e-6, 0.1, luts=luts)
+        assert np.array_equal(masks, g[f"masks{n}"]) and np.array_equal(masks_i, masks)
+        assert np.array_equal(ops, g[f"ops{n}"])
+        for s in range(4):
+            assert O.max_rel_error(pr[s] + 1j * pi[s], g[f"planes{n}"][s]) <= 1e-12
+        # telescoping: == the direct sum of the rotated field
+        assert O.max_rel_error(g[f"tele{n}"], g[f"direct{n}"]) <= 1e-9

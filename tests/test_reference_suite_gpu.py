@@ -265,12 +265,53 @@ def test_pointwise_oracle_synthesis():  # :369-406
     assert O.max_rel_error(hs, hx + hy) <= MAXREL
 
 
-def test_random_phase_is_rejected_loudly():  # :408-433 (complex amplitudes out of scope)
-    n = 16
-    scene = scene_for(n)
-    with pytest.raises(W.ValidationError):
-        W.synthesize_progressive(random_image(n, 13), W.uniform_saliency(n), scene, zero_thresholds(),
-                                 W.LutSet.build(scene), 1, 424242)
+@pytest.mark.parametrize("method", ["lut", "direct", "fft"])
+def test_random_initial_phase_keeps_the_telescoping_identity(method):  # :408-433
+    g = golden("ref_random_phase")
+    for n in (16, 32):
+        scene = scene_for(n)
+        seed = int(g[f"seed{n}"])
+        luts = W.LutSet.build(scene)
+        r = W.synthesize_progressive(g[f"object{n}"], W.uniform_saliency(n), scene,
+                                     zero_thresholds(), luts, 1, seed, method=method)
+        # == the direct Eq.(1) sum of the rotated field (the reference's 1e-9 check)
+        assert O.max_rel_error(r.after_full, g[f"direct{n}"]) <= MAXREL
+        assert O.rel_l2(r.after_full, g[f"tele{n}"]) <= 1e-4
+        assert [r.ops.get(l) for l in W.OpLevel] == list(g[f"tele_ops{n}"])
+        # same seed, same result (worker count is irrelevant on the device)
+        again = W.synthesize_progressive(g[f"object{n}"], W.uniform_saliency(n), scene,
+                                         zero_thresholds(), luts, 2, seed, method=method)
+        assert np.array_equal(again.after_full, r.after_full)
+    # unit-modulus phases preserve the amplitude; the rotation is the reference's own
+    rot = W.random_phase_field(g["object16"], int(g["seed16"]))
+    assert np.array_equal(rot, g["rotated16"])
+    assert np.allclose(np.abs(rot), g["object16"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("method", ["lut", "direct", "fft"])
+def test_random_initial_phase_snapshots_masks_ops_vs_reference(method):  # synthesis.cpp:205-251
+    g = golden("ref_random_phase")
+    for n in (16, 32):
+        scene = scene_for(n)
+        r = W.synthesize_progressive(g[f"object{n}"], g[f"saliency{n}"], scene, W.RefinementPlan(),
+                                     W.LutSet.build(scene), 1, int(g[f"seed{n}"]), method=method)
+        for s, snap in enumerate((r.base_lll, r.after_ll, r.after_l, r.after_full)):
+            assert O.rel_l2(snap, g[f"planes{n}"][s]) <= 1e-4, (n, s)
+            assert O.max_rel_error(snap, g[f"planes{n}"][s]) <= MAXREL, (n, s)
+        masks = np.concatenate([r.mask_ll.on.ravel(), r.mask_l.on.ravel(), r.mask_full.on.ravel()])
+        assert np.array_equal(masks, g[f"masks{n}"])
+        assert [r.ops.get(l) for l in W.OpLevel] == list(g[f"ops{n}"])
+
+
+def test_random_initial_phase_pointwise_oracle():  # synthesis.cpp:255-286 with a seed
+    g = golden("ref_random_phase")
+    for n in (16, 32):
+        scene = scene_for(n)
+        c = W.OpCounter()
+        pw = W.synthesize_pointwise_oracle(g[f"object{n}"], scene, c, W.build_block_lut(scene, 1), 1,
+                                           int(g[f"seed{n}"]))
+        assert O.max_rel_error(pw, g[f"pointwise{n}"]) <= MAXREL
+        assert c.get(W.OpLevel.POINTWISE_ORACLE) == int(g[f"pointwise_ops{n}"])
 
 
 def test_synthesize_progressive_validation():  # :435-451
