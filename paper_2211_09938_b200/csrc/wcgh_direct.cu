@@ -47,22 +47,21 @@ __device__ __forceinline__ float i2f_small(int v) {
   return __int_as_float(v + 0x4B400000) - 12582912.0f;
 }
 
-// Point record as staged in shared memory: (x, y, amplitude bits, phase
-// offset). A complex amplitude a = |a| e^{i psi} (random-initial-phase
-// objects) becomes |a| and psi as a 0.32 fixed-point fraction of a cycle,
-// added to the point's phase: the per-pixel work is the real-amplitude
-// loop. Real points carry psi = 0 (the record's layer field is not needed).
-__device__ __forceinline__ int4 stage_point(const int4* pts, const float* pim, long long i) {
+// Complex amplitudes (random-initial-phase objects): a = |a| e^{i psi} is
+// staged once per launch as the record (x, y, |a|, psi) with psi a 0.32
+// fixed-point fraction of a cycle, added to the point's fixed-point phase
+// (fp64 mode: psi in radians). The per-pixel work is the real kernel's.
+__global__ void k_polar_points(const int4* __restrict__ pts, const float* __restrict__ pim,
+                               long long n, int4* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
   int4 p = pts[i];
-  p.w = 0;
-  if (pim) {
-    const double ar = double(__int_as_float(p.z)), ai = double(pim[i]);
-    double cyc = atan2(ai, ar) * 0.15915494309189533577;  // [-1/2, 1/2]
-    if (cyc < 0.0) cyc += 1.0;
-    p.z = __float_as_int(float(sqrt(ar * ar + ai * ai)));
-    p.w = int(uint32_t(uint64_t(cyc * 4294967296.0 + 0.5)));
-  }
-  return p;
+  const double ar = double(__int_as_float(p.z)), ai = double(pim[i]);
+  double cyc = atan2(ai, ar) * 0.15915494309189533577;  // [-1/2, 1/2]
+  if (cyc < 0.0) cyc += 1.0;
+  p.z = __float_as_int(float(sqrt(ar * ar + ai * ai)));
+  p.w = int(uint32_t(uint64_t(cyc * 4294967296.0 + 0.5)));
+  out[i] = p;
 }
 
 // Chunk c of the point list, restricted to layer l: [s0, s1).
@@ -73,11 +72,13 @@ __device__ __forceinline__ void layer_span(const long long* lb, int l, long long
 }
 
 // NC: phase-series terms (b_2 .. b_{NC+1}); AMP: 0 = MUFU.RSQ, 1/2/3 = degree of
-// the (1+u)^(-1/2) polynomial.
-template <int P, int NC, int AMP, int MINB>
+// the (1+u)^(-1/2) polynomial. CPLX: polar records (k_polar_points) whose
+// w field is a phase offset, a separate instantiation so the real kernel
+// carries no phase-offset code at all.
+template <int P, int NC, int AMP, int MINB, bool CPLX>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k_direct_fixed(const int4* __restrict__ pts, const float* __restrict__ pim,
-                   const long long* __restrict__ layer_begin, int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
+    k_direct_fixed(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
+                   int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                    int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
   const int lane = threadIdx.x & 31;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = stage_point(pts, pim, b + threadIdx.x);
+      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
       __syncthreads();
 
 #pragma unroll 1
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int dy = y - q.y;
         const int s = dx0 * dx0 + dy * dy;  // exact: |dx|,|dy| < 2^15
         const int s_1 = s + 64 * dx0 + 1024;  // pixel i = 1 (x + 32)
-        const uint32_t ph0 = phi0 + uint32_t(q.w);  // + the point's phase offset
+        const uint32_t ph0 = CPLX ? phi0 + uint32_t(q.w) : phi0;  // + the point's phase offset
         uint32_t t = uint32_t(s) * a_hi + __umulhi(uint32_t(s), a_lo) + ph0;
         const uint32_t t1 = uint32_t(s_1) * a_hi + __umulhi(uint32_t(s_1), a_lo) + ph0;
         uint32_t D = t1 - t;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // fp32 sin/cos. Accuracy mode (FP64-pipe bound).
 template <int P>
 __global__ void __launch_bounds__(kThreads)
-    k_direct_fp64(const int4* __restrict__ pts, const float* __restrict__ pim,
+    k_direct_fp64(const int4* __restrict__ pts, bool cplx,
                   const long long* __restrict__ layer_begin, int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                   int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   __shared__ int4 sp[kBatch];
@@ -204,14 +205,14 @@ __global__ void __launch_bounds__(kThreads)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = stage_point(pts, pim, b + threadIdx.x);
+      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
       __syncthreads();
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
         const int4 q = sp[j];
         const double ddy = double(y - q.y) * pitch;
         const double a = double(__int_as_float(q.z));
-        const double psi = double(uint32_t(q.w)) * (two_pi / 4294967296.0);
+        const double psi = cplx ? double(uint32_t(q.w)) * (two_pi / 4294967296.0) : 0.0;
 #pragma unroll
         for (int i = 0; i < P; ++i) {
           const double ddx = double(xb + 32 * i - q.x) * pitch;
@@ -275,7 +276,7 @@ struct LaunchArgs {
   dim3 grid;
   cudaStream_t s;
   const int4* pts;
-  const float* pim;
+  bool cplx;
   const long long* lb;
   int L;
   long long np;
@@ -287,8 +288,12 @@ struct LaunchArgs {
 template <int P, int NC, int AMP>
 void launch_fixed(const LaunchArgs& a) {
   constexpr int MINB = 2;
-  k_direct_fixed<P, NC, AMP, MINB><<<a.grid, kThreads, 0, a.s>>>(
-      a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+  if (a.cplx)
+    k_direct_fixed<P, NC, AMP, MINB, true><<<a.grid, kThreads, 0, a.s>>>(
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+  else
+    k_direct_fixed<P, NC, AMP, MINB, false><<<a.grid, kThreads, 0, a.s>>>(
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
 }
 
 template <int P, int NC>
@@ -421,25 +426,33 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
   const size_t lb_bytes = sizeof(long long) * (n_layers + 1);
   const size_t part_bytes = ((band * group * sizeof(float2)) + 255) / 256 * 256;
   char* base = static_cast<char*>(scratch.partial.reserve(part_bytes + lb_bytes));
+  const int4* pts = reinterpret_cast<const int4*>(pts_dev);
+  int launches = 0;
+  if (pim_dev) {  // complex amplitudes -> polar records
+    int4* polar = static_cast<int4*>(scratch.polar.reserve(sizeof(int4) * size_t(n_points)));
+    k_polar_points<<<unsigned((n_points + 255) / 256), 256, 0, stream>>>(pts, pim_dev, n_points, polar);
+    WCGH_CHECK_LAUNCH();
+    pts = polar;
+    launches += 1;
+  }
   long long* lb_dev = reinterpret_cast<long long*>(base + part_bytes);
   float2* partial = reinterpret_cast<float2*>(base);
   static_assert(sizeof(long long) == sizeof(int64_t), "int64");
   WCGH_CUDA(cudaMemcpyAsync(lb_dev, layer_begin_host, lb_bytes, cudaMemcpyHostToDevice, stream));
 
-  int launches = 0;
   for (int g0 = 0; g0 < n_chunks; g0 += group) {
     const int ng = std::min(group, n_chunks - g0);
     LaunchArgs a{dim3(unsigned(tiles_x * tiles_y), unsigned(ng)), stream,
-                 reinterpret_cast<const int4*>(pts_dev), pim_dev, lb_dev, n_layers, n_points, g0, nh,
+                 pts, pim_dev != nullptr, lb_dev, n_layers, n_points, g0, nh,
                  row0, rows, tiles_x, partial, band};
     if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), stream));
     if (phase_mode == WCGH_PHASE_FP64) {
       if (P == 32)
-        k_direct_fp64<32><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<32><<<a.grid, kThreads, 0, stream>>>(a.pts, a.cplx, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
       else if (P == 16)
-        k_direct_fp64<16><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<16><<<a.grid, kThreads, 0, stream>>>(a.pts, a.cplx, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
       else
-        k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.pim, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+        k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.cplx, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
     } else {
       if (P == 32)
         launch_fixed_nc<32>(plan, a);

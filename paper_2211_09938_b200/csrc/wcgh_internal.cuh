@@ -154,6 +154,7 @@ DirectLayer make_direct_layer(const wcgh_layer& L);
 // points' imaginary amplitudes (complex objects; pts[i].a is the real part).
 struct DirectScratch {
   DevBuf partial;
+  DevBuf polar;  // complex amplitudes as (x, y, |a|, phase) records
 };
 int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, int n_layers,
                   const wcgh_layer* layers, int nh, int row0, int rows, int phase_mode,
