@@ -91,9 +91,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
   const long long p1 = min(p0 + kChunk, n_points);
 
-  float re[P], im[P];
+  // Pixels are processed in pairs (i, i+1) with packed fp32x2 arithmetic
+  // (FFMA2/FMUL2/FADD2: the same IEEE operation per lane at half the issue
+  // slots), so the per-update instruction stream is 2 MUFU + ~8 issue slots
+  // and the XU pipe is the only bound. re2[k] = (re_{2k}, re_{2k+1}).
+  static_assert(P % 2 == 0, "pixel pairs");
+  float2 re2[P / 2], im2[P / 2];
 #pragma unroll
-  for (int i = 0; i < P; ++i) re[i] = im[i] = 0.0f;
+  for (int i = 0; i < P / 2; ++i) re2[i] = im2[i] = make_float2(0.0f, 0.0f);
 
   for (int l = 0; l < n_layers; ++l) {
     long long s0, s1;
@@ -101,12 +106,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (s0 >= s1) continue;
     const DirectLayer& L = c_layers[l];
     const uint32_t a_hi = L.a_hi, a_lo = L.a_lo, phi0 = L.phi0, dd = L.dd;
+    const uint32_t dd2 = 2u * dd;
     const float c = L.c, inv_z = L.inv_z;
     const float c64 = 64.0f * c, c1024 = 1024.0f * c, ddu = 2048.0f * c;
-    float corr[NC];
+    const float2 ddu4 = make_float2(4.0f * ddu, 4.0f * ddu);
+    float2 corr[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) corr[k] = L.corr[k];
+    for (int k = 0; k < NC; ++k) corr[k] = make_float2(L.corr[k], L.corr[k]);
     const float am1 = L.amp[0], am2 = L.amp[1], am3 = L.amp[2];
+    const float2 two_pi2 = make_float2(kTwoPi, kTwoPi);
+    const float2 neg3pi2 = make_float2(kNegThreePi, kNegThreePi);
 
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
@@ -122,42 +131,54 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int s = dx0 * dx0 + dy * dy;  // exact: |dx|,|dy| < 2^15
         const int s_1 = s + 64 * dx0 + 1024;  // pixel i = 1 (x + 32)
         const uint32_t ph0 = CPLX ? phi0 + uint32_t(q.w) : phi0;  // + the point's phase offset
+        // t_i: fixed-point phase of pixel i; D: t_{i+1} - t_i for the current
+        // pair's first pixel (second difference dd, exact in wrap arithmetic)
         uint32_t t = uint32_t(s) * a_hi + __umulhi(uint32_t(s), a_lo) + ph0;
         const uint32_t t1 = uint32_t(s_1) * a_hi + __umulhi(uint32_t(s_1), a_lo) + ph0;
         uint32_t D = t1 - t;
         const float fdx = i2f_small(dx0), fdy = i2f_small(dy);
-        float u = fmaf(fdx * c, fdx, fdy * fdy * c);
-        float du = fmaf(fdx, c64, c1024);
+        // u_i and its pair increment: u_{i+2} - u_i = 2 du_i + ddu
+        const float u0 = fmaf(fdx * c, fdx, fdy * fdy * c);
+        const float du0 = fmaf(fdx, c64, c1024);
+        float2 U = make_float2(u0, u0 + du0);
+        const float v0 = fmaf(2.0f, du0, ddu);
+        float2 V = make_float2(v0, fmaf(2.0f, ddu, v0));
         const float a0 = __int_as_float(q.z) * inv_z;
-        const float a1 = a0 * am1, a2 = a0 * am2, a3 = a0 * am3;
+        const float2 A0 = make_float2(a0, a0);
+        const float2 A1 = make_float2(a0 * am1, a0 * am1);
+        const float2 A2 = make_float2(a0 * am2, a0 * am2);
+        const float2 A3 = make_float2(a0 * am3, a0 * am3);
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
+        for (int i = 0; i < P / 2; ++i) {
+          const uint32_t ta = t, tb = t + D;
+          t = tb + D + dd;
+          D += dd2;
           // [1,2) cycles from the top 23 fraction bits of the fixed-point phase
-          const float phf = __int_as_float((t >> 9) | 0x3f800000u);
-          const float u2 = u * u;
-          float pc = corr[NC - 1];
+          const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
+                                         __int_as_float((tb >> 9) | 0x3f800000u));
+          const float2 u2 = __fmul2_rn(U, U);
+          float2 pc = corr[NC - 1];
 #pragma unroll
-          for (int k = NC - 2; k >= 0; --k) pc = fmaf(pc, u, corr[k]);
+          for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
           // radians: (phf - 1.5) * 2pi + u^2 * pc (phi0 carries the half cycle)
-          const float ph = fmaf(phf, kTwoPi, fmaf(u2, pc, kNegThreePi));
-          float am;
+          const float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
+          float2 am;
           if constexpr (AMP == 3) {
-            am = fmaf(fmaf(fmaf(a3, u, a2), u, a1), u, a0);
+            am = __ffma2_rn(__ffma2_rn(__ffma2_rn(A3, U, A2), U, A1), U, A0);
           } else if constexpr (AMP == 1) {
-            am = fmaf(a1, u, a0);
+            am = __ffma2_rn(A1, U, A0);
           } else if constexpr (AMP == 2) {
-            am = fmaf(fmaf(a2, u, a1), u, a0);
+            am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
           } else {
-            am = a0 * rsqrtf(1.0f + u);
+            am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
           }
-          float sn, cs;
-          __sincosf(ph, &sn, &cs);
-          re[i] = fmaf(am, cs, re[i]);
-          im[i] = fmaf(am, sn, im[i]);
-          t += D;
-          D += dd;
-          u += du;
-          du += ddu;
+          float2 sn, cs;
+          __sincosf(ph.x, &sn.x, &cs.x);
+          __sincosf(ph.y, &sn.y, &cs.y);
+          re2[i] = __ffma2_rn(am, cs, re2[i]);
+          im2[i] = __ffma2_rn(am, sn, im2[i]);
+          U = __fadd2_rn(U, V);
+          V = __fadd2_rn(V, ddu4);
         }
       }
     }
@@ -168,7 +189,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int x = xb + 32 * i;
-      if (x < nh) dst[x] = make_float2(re[i], im[i]);
+      const float2 r = i & 1 ? make_float2(re2[i / 2].y, im2[i / 2].y)
+                             : make_float2(re2[i / 2].x, im2[i / 2].x);
+      if (x < nh) dst[x] = r;
     }
   }
 }
