@@ -503,7 +503,9 @@ def main():
             per_clk, kernel = MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE, "k_direct_fixed (K3)"
             basis = (f"canonical SFU roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz (MEASURED_PEAKS "
                      "sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)); the kernel "
-                     "issues 2 MUFU + ~15 FMA/ALU per update; not an HBM or tensor-core kernel")
+                     "issues 2 MUFU + ~8.5 packed-fp32x2/ALU issue slots per update, so its own "
+                     "bound is 2 MUFU per update (frac_of_2mufu_bound); not an HBM or "
+                     "tensor-core kernel")
             bound = "sfu"
             dram = int(points * 16 + rows * c.plane_size * 8)
         elif job.spec.method == "lut":
@@ -538,6 +540,8 @@ def main():
                                        if f_meas and per_clk else None),
             "dram_bytes_per_step_algorithmic": dram,
         }
+        if bound == "sfu":  # the XU bound of the kernel's actual 2-MUFU instruction mix
+            roof["frac_of_2mufu_bound"] = achieved / (SM_COUNT * f_max * MUFU_PER_CLK_SM / 2.0)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
