@@ -326,6 +326,15 @@ LutVariant lut_variant() {
   }();
   return v;
 }
+// Largest gap (in cell rows) a run steps through with zero weights; a wider
+// gap starts a new run (window reload). WCGH_LUT_GAP overrides (tuning).
+int lut_gap() {
+  static const int g = [] {
+    const char* e = std::getenv("WCGH_LUT_GAP");
+    return e ? std::max(1, std::atoi(e)) : lut_variant().R;
+  }();
+  return g;
+}
 int lut_chunk_target() {
   static const int t = [] {
     const char* e = std::getenv("WCGH_LUT_CHUNKS");
@@ -394,7 +403,7 @@ int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t s) {
   sc.dense.reserve(sizeof(float) * (mm + 1));
   WCGH_CUDA(cudaMemsetAsync(sc.dense.p, 0, sizeof(float) * (mm + 1), s));
   const unsigned g = unsigned((m + 7) / 8);
-  const int R = lut_variant().R;
+  const int R = lut_gap();
   sc.gap = R;
   k_runs_count<<<g, 256, 0, s>>>(w, m, R, c, c + (m + 1), c + 2 * (m + 1));
   WCGH_CHECK_LAUNCH();
@@ -422,7 +431,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   }
   // chunk size depends on the stage's step count only (never on the row band)
   const LutVariant v = lut_variant();
-  require(sc.gap == v.R, "LUT superposition: run lists built for another window height");
+  require(sc.gap >= 1, "LUT superposition: run lists not built");
   require(block * v.R * v.W <= kLutGuardAfter - 16 && block * (v.D + 1) + 1 <= kLutGuardBefore,
           "LUT superposition: window shape exceeds the LUT guard rows");
   const int target = lut_chunk_target();
