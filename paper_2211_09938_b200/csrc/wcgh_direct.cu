@@ -283,6 +283,27 @@ __global__ void k_reduce_chunks(const float2* __restrict__ partial, int n_chunks
   store_peers(peers, i, r);  // fused row-tile gather (last chunk group only)
 }
 
+// The same reduction two pixels per thread: float4 loads of the partials and
+// float4 complex64 stores of the plane (and of the peer planes), bitwise
+// equal to k_reduce_chunks (same per-pixel order).
+__global__ void k_reduce_chunks2(const float4* __restrict__ partial, int n_chunks, size_t count2,
+                                 int accumulate, float4* __restrict__ out, PeerPlanes peers) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count2) return;
+  double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+  if (accumulate) {
+    const float4 o = out[i];
+    r0 = o.x, i0 = o.y, r1 = o.z, i1 = o.w;
+  }
+  for (int c = 0; c < n_chunks; ++c) {
+    const float4 v = partial[size_t(c) * count2 + i];
+    r0 += v.x, i0 += v.y, r1 += v.z, i1 += v.w;
+  }
+  const float4 r = make_float4(float(r0), float(i0), float(r1), float(i1));
+  out[i] = r;
+  store_peers2(peers, 2 * i, r);  // fused row-tile gather (last chunk group only)
+}
+
 __global__ void k_band_to_peers(const float2* __restrict__ band, size_t count, PeerPlanes peers) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < count) store_peers(peers, i, band[i]);
@@ -487,8 +508,14 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     WCGH_CHECK_LAUNCH();
     if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), stream));
     const bool last = g0 + ng >= n_chunks;
-    k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(
-        partial, ng, band, g0 > 0, out_dev, last && peers ? *peers : PeerPlanes{});
+    const PeerPlanes pp = last && peers ? *peers : PeerPlanes{};
+    if (band % 2 == 0 && reinterpret_cast<uintptr_t>(out_dev) % 16 == 0 && peers_aligned16(pp))
+      k_reduce_chunks2<<<unsigned((band / 2 + 255) / 256), 256, 0, stream>>>(
+          reinterpret_cast<const float4*>(partial), ng, band / 2, g0 > 0,
+          reinterpret_cast<float4*>(out_dev), pp);
+    else
+      k_reduce_chunks<<<unsigned((band + 255) / 256), 256, 0, stream>>>(partial, ng, band, g0 > 0,
+                                                                        out_dev, pp);
     WCGH_CHECK_LAUNCH();
     launches += 2;
   }

@@ -84,6 +84,18 @@ __global__ void k_extract(const float2* __restrict__ grid, int L, int nh, int ro
   store_peers(peers, i, r);  // fused row-tile gather
 }
 
+// Two pixels per thread (nh and L even): float4 grid loads, float4 complex64 stores.
+__global__ void k_extract2(const float4* __restrict__ grid, int L2h, int nh2, int row0, int rows,
+                           float scale, float4* __restrict__ out, PeerPlanes peers) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= size_t(rows) * nh2) return;
+  const int x = int(i % nh2), y = int(i / nh2);
+  const float4 v = grid[size_t(row0 + y) * L2h + x];
+  const float4 r = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
+  out[i] = r;
+  store_peers2(peers, 2 * i, r);  // fused row-tile gather
+}
+
 inline unsigned blocks_for(size_t n) { return unsigned((n + 255) / 256); }
 
 // WCGH_SYNC_DEBUG=1: synchronize after every step and name the failing one.
@@ -149,9 +161,15 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
   WCGH_CUFFT(cufftExecC2C(fp.plan, reinterpret_cast<cufftComplex*>(acc),
                           reinterpret_cast<cufftComplex*>(acc), CUFFT_INVERSE));
   dbg(s, "inverse_fft");
-  k_extract<<<blocks_for(size_t(rows) * nh), 256, 0, s>>>(acc, L, nh, row0, rows,
-                                                          float(1.0 / double(L2)), out,
-                                                          peers ? *peers : PeerPlanes{});
+  const PeerPlanes pp = peers ? *peers : PeerPlanes{};
+  if (nh % 2 == 0 && L % 2 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(acc) % 16 == 0 && peers_aligned16(pp))
+    k_extract2<<<blocks_for(size_t(rows) * nh / 2), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(acc), L / 2, nh / 2, row0, rows, float(1.0 / double(L2)),
+        reinterpret_cast<float4*>(out), pp);
+  else
+    k_extract<<<blocks_for(size_t(rows) * nh), 256, 0, s>>>(acc, L, nh, row0, rows,
+                                                            float(1.0 / double(L2)), out, pp);
   WCGH_CHECK_LAUNCH();
   if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
   return launches + 2;

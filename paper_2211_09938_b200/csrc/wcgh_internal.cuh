@@ -78,6 +78,16 @@ struct PeerPlanes {
 __device__ __forceinline__ void store_peers(const PeerPlanes& pp, size_t i, float2 v) {
   for (int k = 0; k < pp.n; ++k) pp.p[k][pp.offset + i] = v;
 }
+// two adjacent pixels (i even, offset even, peer planes 16-byte aligned) as one float4
+__device__ __forceinline__ void store_peers2(const PeerPlanes& pp, size_t i, float4 v) {
+  for (int k = 0; k < pp.n; ++k) *reinterpret_cast<float4*>(pp.p[k] + pp.offset + i) = v;
+}
+inline bool peers_aligned16(const PeerPlanes& pp) {
+  if (pp.offset % 2) return false;
+  for (int k = 0; k < pp.n; ++k)
+    if (reinterpret_cast<uintptr_t>(pp.p[k]) % 16) return false;
+  return true;
+}
 
 // copy a finished band into the peer planes (used where no fused epilogue exists)
 int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes& peers,

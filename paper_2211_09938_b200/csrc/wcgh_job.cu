@@ -266,6 +266,35 @@ __global__ void k_sum_stages(const float2* __restrict__ planes, size_t count, in
   store_peers(peers, i, make_float2(re, im));  // fused row-tile gather (job run only)
 }
 
+// Two pixels per thread: float4 loads of the stage planes, float4 complex64
+// stores of the plane and the peer planes (same per-pixel order, bitwise equal).
+__global__ void k_sum_stages2(const float4* __restrict__ planes, size_t count2, int n_stages,
+                              float4* __restrict__ out, PeerPlanes peers) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count2) return;
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int st = 0; st < n_stages; ++st) {
+    const float4 v = planes[size_t(st) * count2 + i];
+    r.x += v.x;
+    r.y += v.y;
+    r.z += v.z;
+    r.w += v.w;
+  }
+  out[i] = r;
+  store_peers2(peers, 2 * i, r);
+}
+
+void launch_sum_stages(const float2* planes, size_t band, int n_stages, float2* out,
+                       const PeerPlanes& peers, cudaStream_t s) {
+  if (band % 2 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(planes) % 16 == 0 && peers_aligned16(peers))
+    k_sum_stages2<<<unsigned((band / 2 + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(planes), band / 2, n_stages, reinterpret_cast<float4*>(out), peers);
+  else
+    k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(planes, band, n_stages, out, peers);
+  WCGH_CHECK_LAUNCH();
+}
+
 void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
   const wcgh_desc& d = j->desc;
   const int No = d.object_size, L = d.n_layers;
@@ -338,9 +367,7 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
     }
   j->stats.synth_launches = j->timing.launches();
   WCGH_CUDA(cudaEventRecord(j->ev[2], s));
-  k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(sp, band, 4, j->plane.as<float2>(),
-                                                            j->peers);
-  WCGH_CHECK_LAUNCH();
+  launch_sum_stages(sp, band, 4, j->plane.as<float2>(), j->peers, s);
   j->stats.total_launches += 1;
   WCGH_CUDA(cudaEventRecord(j->ev[3], s));
   sync(s);
@@ -572,9 +599,7 @@ int wcgh_job_download_stages(wcgh_job* job, float* out4) {
     float2* tmp = static_cast<float2*>(job->lut_scratch.reserve(sizeof(float2) * band));
     for (int st = 0; st < 4; ++st) {
       // snapshot after stage st = sum of stage planes 0..st, in stage order
-      k_sum_stages<<<unsigned((band + 255) / 256), 256, 0, s>>>(job->stage_planes.as<float2>(), band,
-                                                                st + 1, tmp, PeerPlanes{});
-      WCGH_CHECK_LAUNCH();
+      launch_sum_stages(job->stage_planes.as<float2>(), band, st + 1, tmp, PeerPlanes{}, s);
       WCGH_CUDA(cudaMemcpyAsync(out4 + 2 * band * st, tmp, sizeof(float2) * band, cudaMemcpyDeviceToHost, s));
       sync(s);
     }
