@@ -238,9 +238,10 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
     // prefetch pointer: diagonal -(D + 1), then one row lower per step
     const float2* pf = rp - (D + 1) * row_step;
     // one step: MAC the listed weight (zero in gaps), then refill the dead slot
-#define WCGH_LUT_STEP(uu, u)                                                    \
+#define WCGH_LUT_STEP(uu, u) WCGH_LUT_STEP_W(uu, ws[u])
+#define WCGH_LUT_STEP_W(uu, wexpr)                                              \
   {                                                                             \
-    const float wv = ws[u];                                                     \
+    const float wv = (wexpr);                                                   \
     if (wv != 0.f) {                                                            \
       _Pragma("unroll") for (int j = 0; j < R; ++j)                             \
       _Pragma("unroll") for (int i = 0; i < PX; ++i) {                          \
@@ -256,10 +257,19 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
 #pragma unroll
       for (int uu = 0; uu < S; ++uu) WCGH_LUT_STEP(uu, ub + uu)
     }
+    // remainder (< S steps): weights read up front (the shared array has
+    // >= 32 slack slots past the chunk's last run), one uniform branch per step
+    const int rem = n_steps - full;
+    if (rem > 0) {
+      float wt[S - 1];
 #pragma unroll
-    for (int uu = 0; uu < S - 1; ++uu) {
-      if (full + uu < n_steps) WCGH_LUT_STEP(uu, full + uu)
+      for (int k = 0; k < S - 1; ++k) wt[k] = ws[full + k];
+#pragma unroll
+      for (int uu = 0; uu < S - 1; ++uu) {
+        if (uu < rem) WCGH_LUT_STEP_W(uu, wt[uu])
+      }
     }
+#undef WCGH_LUT_STEP_W
 #undef WCGH_LUT_STEP
   }
 
