@@ -18,6 +18,7 @@ Rules (BASELINE.json configs):
 """
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -110,3 +111,24 @@ def make_scene(cfg: int | SceneConfig, saliency_frac: float | None = None,
         mseed = 2000 + 10 * c.cfg + (0 if c.cfg == 4 else layer)
         masks.append(smooth_mask(c.object_size, mseed, c.saliency_frac))
     return Scene(c, np.stack(objs), np.stack(masks))
+
+
+def scene_digest(scene: Scene) -> dict:
+    """SHA-256 of the object and mask bytes plus the realised fractions, so
+    the CPU oracle, the GPU box and the committed fixtures can be shown to use
+    byte-identical inputs (tests/golden/scene_digests.json)."""
+    o, m = np.ascontiguousarray(scene.objects), np.ascontiguousarray(scene.masks)
+    return {
+        "objects_sha256": hashlib.sha256(o.tobytes()).hexdigest(),
+        "masks_sha256": hashlib.sha256(m.tobytes()).hexdigest(),
+        "shape": list(o.shape),
+        "nonzero_frac": float(np.count_nonzero(o) / o.size),
+        "salient_frac": float(np.count_nonzero(m) / m.size),
+    }
+
+
+def digest_cases() -> list[tuple[str, int, float | None]]:
+    """(name, cfg, saliency_frac) of every BASELINE config, cfg4 per sweep point."""
+    cases = [(CONFIGS[c].name, c, None) for c in (0, 1, 2, 3)]
+    cases += [(f"{CONFIGS[4].name}_sal{f:.2f}", 4, f) for f in (0.0, 0.10, 0.25, 0.50, 1.0)]
+    return cases
