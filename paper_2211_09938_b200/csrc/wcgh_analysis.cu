@@ -726,6 +726,10 @@ __device__ __forceinline__ void cell_u8(const uint2 (&ov)[8], const uint2 (&sv)[
   n_f = __reduce_add_sync(kFull, n_f);
   if (lane == 0 && n_b) {
     unsigned long long* ops = out.ops + layer * WCGH_OP_LEVELS;
+    if (out.ops_rep) {  // one of kOpReplicas copies, by warp
+      const unsigned wid = (blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+      ops = out.ops_rep + (size_t(wid % kOpReplicas) * gridDim.z + layer) * WCGH_OP_LEVELS;
+    }
     atomicAdd(ops + WCGH_OP_BASE_LLL, (unsigned long long)n_b);
     if (n_ll) atomicAdd(ops + WCGH_OP_REFINE_LL, (unsigned long long)n_ll);
     if (n_l) atomicAdd(ops + WCGH_OP_REFINE_L, (unsigned long long)n_l);
@@ -778,6 +782,34 @@ __global__ void __launch_bounds__(kU8Threads, MINB) k_analysis_u8(const uint8_t*
     if (by0 + k < m3) cell_u8<WSTAGE>(ov[k], sv[k], bx, by0 + k, bx < m3, n, layer, cut, out);
 }
 
+// ops[layer][k] += sum over replicas of ops_rep[r][layer][k]; replicas re-zeroed.
+__global__ void __launch_bounds__(256) k_fold_ops(unsigned long long* __restrict__ rep, int n_layers,
+                                                  unsigned long long* __restrict__ ops) {
+  __shared__ unsigned long long s_sum[WCGH_OP_LEVELS][8];
+  const int layer = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long acc[WCGH_OP_LEVELS] = {};
+  for (int r = threadIdx.x; r < kOpReplicas; r += blockDim.x) {
+    unsigned long long* p = rep + (size_t(r) * n_layers + layer) * WCGH_OP_LEVELS;
+#pragma unroll
+    for (int k = 0; k < WCGH_OP_LEVELS; ++k) {
+      acc[k] += p[k];
+      p[k] = 0ull;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < WCGH_OP_LEVELS; ++k) {
+    unsigned long long v = acc[k];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) s_sum[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < WCGH_OP_LEVELS) {
+    unsigned long long v = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) v += s_sum[threadIdx.x][w];
+    ops[size_t(layer) * WCGH_OP_LEVELS + threadIdx.x] += v;
+  }
+}
+
 template <bool WSTAGE>
 void launch_u8(const void* obj, const void* sal, int n, int n_layers, const U8Cuts& cut,
                const AnalysisOut& out, cudaStream_t s) {
@@ -786,6 +818,10 @@ void launch_u8(const void* obj, const void* sal, int n, int n_layers, const U8Cu
             unsigned(n_layers));
   k_analysis_u8<WSTAGE, kCells, 4><<<grid, kU8Threads, 0, s>>>(
       static_cast<const uint8_t*>(obj), static_cast<const uint8_t*>(sal), n, cut, out);
+  if (out.ops_rep) {
+    WCGH_CHECK_LAUNCH();
+    k_fold_ops<<<unsigned(n_layers), 256, 0, s>>>(out.ops_rep, n_layers, out.ops);
+  }
 }
 
 // smallest u8 value v with v * (1/255) > t in fp64 (load_sal's expression)
@@ -830,7 +866,7 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
     else
       launch_u8<false>(obj, sal, n, n_layers, cut, out, s);
     WCGH_CHECK_LAUNCH();
-    return 1;
+    return out.ops_rep ? 2 : 1;
   }
   switch (obj_dtype) {
     case WCGH_U8: dispatch_sal<uint8_t>(obj, obj_scale, sal, sal_dtype, n, n_layers, plan, out, s); break;

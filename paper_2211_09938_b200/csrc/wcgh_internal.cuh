@@ -174,6 +174,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
 
 // ---- analysis (K1 + K2) ----------------------------------------------------
 
+constexpr int kOpReplicas = 256;
 struct AnalysisOut {
   // device outputs (nullptr = not requested), per layer strided by n^2-type sizes
   double* pyramid = nullptr;  // layer stride: pyr_len(n)
@@ -183,6 +184,11 @@ struct AnalysisOut {
   float* w_stage = nullptr;   // LUT weights: base (n/8)^2, ll (n/4)^2, l (n/2)^2, full n^2
   int* seg_counts = nullptr;  // nonzero A_eff per (layer, row, 128-px segment)
   unsigned long long* ops = nullptr;  // per layer 5 counters (device)
+  // optional: kOpReplicas x layers x 5 zeroed partial counters. The uint8 K1
+  // spreads its per-warp counts over them (same-address atomics from every
+  // warp serialised in L2: 25% of the front end at 16384^2) and a fold
+  // kernel adds them into `ops` and re-zeroes them.
+  unsigned long long* ops_rep = nullptr;
   int* err = nullptr;                 // validation flags (device)
 };
 

@@ -67,6 +67,8 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     j->seg_counts.reserve((nseg + 1) * 4);
     j->seg_offsets.reserve((nseg + 1) * 4);
     j->ops.reserve(sizeof(unsigned long long) * WCGH_OP_LEVELS * L + 64);
+    j->ops_rep.reserve(sizeof(unsigned long long) * WCGH_OP_LEVELS * L * kOpReplicas);
+    WCGH_CUDA(cudaMemset(j->ops_rep.p, 0, sizeof(unsigned long long) * WCGH_OP_LEVELS * L * kOpReplicas));
     j->err.reserve(64);
     j->plane.reserve(sizeof(float2) * size_t(d.rows) * d.plane_size);
     WCGH_CUDA(cudaMallocHost(&j->h_offsets, sizeof(int64_t) * (L + 1)));
@@ -156,9 +158,10 @@ void run_analysis(wcgh_job* j, cudaStream_t s, bool lut) {
   ao.seg_counts = (lut || cplx) ? nullptr : j->seg_counts.as<int>();
   ao.w_stage = lut ? j->w_stage.as<float>() : nullptr;
   ao.ops = j->ops.as<unsigned long long>();
+  ao.ops_rep = j->ops_rep.as<unsigned long long>();  // zeroed at creation, re-zeroed by the fold
   ao.err = reinterpret_cast<int*>(ao.ops + WCGH_OP_LEVELS * L);
-  launch_analysis(j->obj.p, d.obj_dtype, d.obj_scale, j->sal.p, d.sal_dtype, No, L, d.plan, ao, s);
-  j->stats.total_launches += 1;
+  j->stats.total_launches +=
+      launch_analysis(j->obj.p, d.obj_dtype, d.obj_scale, j->sal.p, d.sal_dtype, No, L, d.plan, ao, s);
   if (!cplx) return;
   AnalysisOut bo = ao;
   bo.a_eff = static_cast<float*>(j->a_eff_im.reserve(sizeof(float) * j->in_elems * L));
@@ -166,9 +169,9 @@ void run_analysis(wcgh_job* j, cudaStream_t s, bool lut) {
                    : nullptr;
   bo.ops = static_cast<unsigned long long*>(j->ops_im.reserve(ops_bytes));
   WCGH_CUDA(cudaMemsetAsync(bo.ops, 0, ops_bytes, s));
-  launch_analysis(static_cast<const char*>(j->obj.p) + sizeof(double), d.obj_dtype, d.obj_scale,
-                  j->sal.p, d.sal_dtype, No, L, d.plan, bo, s);
-  j->stats.total_launches += 1;
+  j->stats.total_launches +=
+      launch_analysis(static_cast<const char*>(j->obj.p) + sizeof(double), d.obj_dtype, d.obj_scale,
+                      j->sal.p, d.sal_dtype, No, L, d.plan, bo, s);
   if (!lut) {
     launch_seg_counts_f32(ao.a_eff, No, L, j->seg_counts.as<int>(), s, bo.a_eff);
     j->stats.total_launches += 1;

@@ -38,7 +38,7 @@ struct wcgh_job {
   std::vector<wcgh_layer> layers;
   int off = 0;
   size_t in_elems = 0;  // per layer No^2
-  wcgh::DevBuf obj, sal, a_eff, seg_counts, seg_offsets, scan_scratch, ops, err, points, plane;
+  wcgh::DevBuf obj, sal, a_eff, seg_counts, seg_offsets, scan_scratch, ops, ops_rep, err, points, plane;
   // LUT method
   wcgh::DevBuf w_stage, stage_planes, lut_scratch, lut_partial;
   std::vector<std::unique_ptr<wcgh::StageCells>> cells;  // [layer * 4 + stage]
