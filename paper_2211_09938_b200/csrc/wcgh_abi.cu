@@ -228,6 +228,9 @@ int wcgh_analyze(wcgh_ctx* ctx, const void* object, int obj_dtype, double obj_sc
     ao.ops = ops;
     ao.err = reinterpret_cast<int*>(ops + WCGH_OP_LEVELS);
     WCGH_CUDA(cudaMemsetAsync(ops, 0, 64, s));
+    const size_t rep_bytes = sizeof(unsigned long long) * WCGH_OP_LEVELS * kOpReplicas;
+    ao.ops_rep = static_cast<unsigned long long*>(ctx->b_ops_rep.reserve(rep_bytes));
+    WCGH_CUDA(cudaMemsetAsync(ao.ops_rep, 0, rep_bytes, s));
     launch_analysis(in, obj_dtype, obj_scale, in + n2 * os, sal_dtype, n, 1, *plan, ao, s);
     launch_scan(ao.seg_counts, seg_off, int(nseg), s, &ctx->b_scan);
     unsigned long long h_ops[WCGH_OP_LEVELS];

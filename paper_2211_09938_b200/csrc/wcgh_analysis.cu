@@ -260,6 +260,10 @@ __global__ void __launch_bounds__(256) k_analysis(const TO* __restrict__ obj, do
   const int anyerr = __reduce_or_sync(kFull, err);
   if (lane == 0 && vmask) {
     unsigned long long* ops = out.ops + layer * WCGH_OP_LEVELS;
+    if (out.ops_rep) {  // replicated counters, folded by k_fold_ops (see AnalysisOut)
+      const unsigned wid = (blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+      ops = out.ops_rep + (size_t(wid % kOpReplicas) * gridDim.z + layer) * WCGH_OP_LEVELS;
+    }
     if (c_base) atomicAdd(ops + WCGH_OP_BASE_LLL, (unsigned long long)c_base);
     if (c_ll) atomicAdd(ops + WCGH_OP_REFINE_LL, (unsigned long long)c_ll);
     if (c_l) atomicAdd(ops + WCGH_OP_REFINE_L, (unsigned long long)c_l);
@@ -838,6 +842,10 @@ void launch_k1(const void* obj, double scale, const void* sal, int n, int n_laye
   dim3 grid((n + 127) / 128, n / 8, n_layers);
   k_analysis<TO, TS><<<grid, 256, 0, s>>>(static_cast<const TO*>(obj), scale,
                                           static_cast<const TS*>(sal), n, plan, out);
+  if (out.ops_rep) {
+    WCGH_CHECK_LAUNCH();
+    k_fold_ops<<<unsigned(n_layers), 256, 0, s>>>(out.ops_rep, n_layers, out.ops);
+  }
 }
 
 template <typename TO>
@@ -876,7 +884,7 @@ int launch_analysis(const void* obj, int obj_dtype, double obj_scale, const void
     default: throw ValidationError("object dtype must be WCGH_U8, WCGH_F32, WCGH_F64 or WCGH_C128");
   }
   WCGH_CHECK_LAUNCH();
-  return 1;
+  return out.ops_rep ? 2 : 1;
 }
 
 int launch_scan(const int* counts, int* offsets, int count, cudaStream_t s, DevBuf* scratch) {

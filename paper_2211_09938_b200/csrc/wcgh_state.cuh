@@ -28,7 +28,7 @@ struct wcgh_ctx {
   wcgh::DirectScratch direct;
   wcgh::StageCells cells;
   wcgh::ReconPlan recon;  // reconstruction / FFT entry points
-  wcgh::DevBuf b_ssim, b_scan;
+  wcgh::DevBuf b_ssim, b_scan, b_ops_rep;
   std::mutex mu;
 };
 
