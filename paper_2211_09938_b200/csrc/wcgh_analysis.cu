@@ -385,18 +385,18 @@ __global__ void __launch_bounds__(1024) k_scan_add(int* __restrict__ offsets, in
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets[count] = aux_ofs[nb];
 }
 
-// Ordered compaction: one warp per (layer, row, 128-pixel segment); lane l
-// owns pixels 4l..4l+3 of the segment (one float4 load). The segment's point
-// records are assembled in shared memory and written as one contiguous,
-// coalesced run of 16-byte stores.
+// Ordered compaction: one warp per (layer, row, 128-pixel segment), in four
+// rounds of 32 pixels (lane l looks at pixel 32k + l: coalesced 128-B loads).
+// Per round a ballot of the nonzero pixels gives each one its rank, and the
+// round's records are stored straight to global memory as one contiguous run
+// of 16-byte stores -- ascending pixel order is the lane order, so the
+// row-major point order is kept without a shared-memory staging pass.
 __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict__ a_eff,
                                                         const float* __restrict__ a_im,
                                                         const int* __restrict__ offsets, int n,
                                                         int n_layers, int off, int layer0,
                                                         wcgh_point* __restrict__ points,
                                                         float* __restrict__ p_im) {
-  __shared__ int4 stage[8][128];
-  __shared__ float stage_im[8][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int segs = seg_per_row(n);
   const long long gw = (long long)blockIdx.x * 8 + warp;
@@ -406,45 +406,32 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
   const long long lr = gw / segs;
   const int row = int(lr % n);
   const int layer = int(lr / n);
-  const float* src = a_eff + (size_t(layer) * n + row) * n;
-  const int x0 = seg * 128 + 4 * lane;
-  float v[4];
-  if (x0 + 3 < n && (n & 3) == 0) {
-    const float4 f = *reinterpret_cast<const float4*>(src + x0);
-    v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (x0 + k < n) ? src[x0 + k] : 0.0f;
-  }
-  float w[4] = {0.f, 0.f, 0.f, 0.f};  // imaginary parts (complex objects)
-  if (a_im) {
-    const float* srci = a_im + (size_t(layer) * n + row) * n;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] = (x0 + k < n) ? srci[x0 + k] : 0.0f;
-  }
-  int nz = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) nz += v[k] != 0.0f || w[k] != 0.0f;
-  int incl = nz;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int seg_total = __shfl_sync(kFull, incl, 31);
-  int pos = incl - nz;
+  const size_t rbase = (size_t(layer) * n + row) * n;
+  const float* src = a_eff + rbase;
+  const float* srci = a_im ? a_im + rbase : nullptr;
   const int py = row + off, pl = layer0 + layer;
+  const unsigned lt = (1u << lane) - 1u;
+  float v[4], w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // all four rounds' loads first
+    const int x = seg * 128 + 32 * k + lane;
+    v[k] = x < n ? src[x] : 0.0f;
+    w[k] = srci && x < n ? srci[x] : 0.0f;
+  }
+  int4* dst = reinterpret_cast<int4*>(points) + offsets[gw];
+  float* dst_im = p_im ? p_im + offsets[gw] : nullptr;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (v[k] != 0.0f || w[k] != 0.0f) {
-      stage_im[warp][pos] = w[k];
-      stage[warp][pos++] = make_int4(x0 + k + off, py, __float_as_int(v[k]), pl);
+    const bool nz = v[k] != 0.0f || w[k] != 0.0f;
+    const unsigned b = __ballot_sync(kFull, nz);
+    if (nz) {
+      const int r = __popc(b & lt);
+      dst[r] = make_int4(seg * 128 + 32 * k + lane + off, py, __float_as_int(v[k]), pl);
+      if (dst_im) dst_im[r] = w[k];
     }
+    dst += __popc(b);
+    if (dst_im) dst_im += __popc(b);
   }
-  __syncwarp();
-  int4* dst = reinterpret_cast<int4*>(points) + offsets[gw];
-  for (int i = lane; i < seg_total; i += 32) dst[i] = stage[warp][i];
-  if (p_im)
-    for (int i = lane; i < seg_total; i += 32) p_im[offsets[gw] + i] = stage_im[warp][i];
 }
 
 // Stage contribution images for the snapshots of the direct and FFT
