@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
         for (int i = 0; i < P / 2; ++i) {
           const uint32_t ta = t, tb = t + D;
-          t = tb + D + dd;
+          // t_{i+2} = t_{i+1} + D + dd as one three-input add (IADD3)
+          asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(t) : "r"(tb), "r"(D), "r"(dd));
           D += dd2;
           // [1,2) cycles from the top 23 fraction bits of the fixed-point phase
           const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
