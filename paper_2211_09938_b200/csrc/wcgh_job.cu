@@ -68,7 +68,9 @@ int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out) {
     j->seg_offsets.reserve((nseg + 1) * 4);
     j->ops.reserve(sizeof(unsigned long long) * WCGH_OP_LEVELS * L + 64);
     j->ops_rep.reserve(sizeof(unsigned long long) * WCGH_OP_LEVELS * L * kOpReplicas);
-    WCGH_CUDA(cudaMemset(j->ops_rep.p, 0, sizeof(unsigned long long) * WCGH_OP_LEVELS * L * kOpReplicas));
+    WCGH_CUDA(cudaMemsetAsync(j->ops_rep.p, 0, sizeof(unsigned long long) * WCGH_OP_LEVELS * L * kOpReplicas,
+                              ctx->stream));
+    sync(ctx->stream);  // zeroed before any stream the job later runs on
     j->err.reserve(64);
     j->plane.reserve(sizeof(float2) * size_t(d.rows) * d.plane_size);
     WCGH_CUDA(cudaMallocHost(&j->h_offsets, sizeof(int64_t) * (L + 1)));
