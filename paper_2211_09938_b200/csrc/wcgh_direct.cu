@@ -35,7 +35,7 @@ __constant__ DirectLayer c_layers[kMaxLayers];
 
 namespace {
 
-constexpr int kBatch = 256;
+constexpr int kBatch = 1024;  // = kChunk: one staging pass per chunk and layer
 constexpr int kThreads = 256;
 constexpr long long kChunk = 1024;          // points per partial sum
 constexpr size_t kPartialBytes = 2ull << 30;  // partial-plane budget per launch group
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
+      for (int i = threadIdx.x; i < nb; i += kThreads) sp[i] = pts[b + i];
       __syncthreads();
 
 #pragma unroll 1
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      if (threadIdx.x < nb) sp[threadIdx.x] = pts[b + threadIdx.x];
+      for (int i = threadIdx.x; i < nb; i += kThreads) sp[i] = pts[b + i];
       __syncthreads();
 #pragma unroll 1
       for (int j = 0; j < nb; ++j) {
