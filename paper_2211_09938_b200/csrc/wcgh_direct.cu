@@ -6,8 +6,9 @@
 //
 // Work decomposition: a CTA of 8 warps owns an 8-row x 32P-column tile; lane
 // l of warp w owns pixels (x_b + l + 32 i, y_0 + w), i < P, and keeps their
-// complex sums in registers. Points stream through shared memory in batches
-// of 256 16-byte records and are broadcast to all threads. The point list is
+// complex sums in registers. Points stream through shared memory (a CTA's
+// whole chunk of 16-byte records per layer span) and are broadcast to all
+// threads. The point list is
 // cut into fixed chunks of kChunk points (boundaries depend on nothing but
 // the point index); each (tile, chunk) CTA writes its chunk's partial sum and
 // a reduction adds the partials in chunk order. The per-pixel summation
