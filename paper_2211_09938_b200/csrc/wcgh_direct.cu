@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int i = threadIdx.x; i < nb; i += kThreads) sp[i] = pts[b + i];
       __syncthreads();
 
-#pragma unroll 1
+#pragma unroll 2
       for (int j = 0; j < nb; ++j) {
         const int4 q = sp[j];
         const int dx0 = xb - q.x;
