@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "wcgh_internal.cuh"
 
@@ -39,7 +40,6 @@ namespace {
 constexpr int kBatch = 1024;  // = kChunk: one staging pass per chunk and layer
 constexpr int kThreads = 256;
 constexpr long long kChunk = 1024;          // points per partial sum
-constexpr size_t kPartialBytes = 2ull << 30;  // partial-plane budget per launch group
 constexpr float kTwoPi = 6.283185307179586f;
 constexpr float kNegThreePi = -9.42477796076938f;
 
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int i = 0; i < P / 2; ++i) {
           const uint32_t ta = t, tb = t + D;
           // t_{i+2} = t_{i+1} + D + dd as one three-input add (IADD3)
-          asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(t) : "r"(tb), "r"(D), "r"(dd));
+          asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=&r"(t) : "r"(tb), "r"(D), "r"(dd));
           D += dd2;
           // [1,2) cycles from the top 23 fraction bits of the fixed-point phase
           const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
@@ -465,7 +465,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
                                     cudaMemcpyHostToDevice, stream));
 
   const int n_chunks = int((n_points + kChunk - 1) / kChunk);
-  const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
+  const int group = partial_group(n_chunks, nh);
   const int P = pixels_per_thread(nh);
   const int tiles_x = (nh + 32 * P - 1) / (32 * P);
   const int tiles_y = (rows + 7) / 8;
@@ -522,6 +522,16 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     launches += 2;
   }
   return launches;
+}
+
+int partial_group(int n_chunks, int nh) {
+  static const size_t budget = [] {
+    size_t b = 2ull << 30;
+    if (const char* e = std::getenv("WCGH_PARTIAL_BYTES")) b = size_t(std::strtoull(e, nullptr, 10));
+    return b;
+  }();
+  const size_t plane = size_t(nh) * size_t(nh) * sizeof(float2);
+  return int(std::max<size_t>(1, std::min<size_t>(size_t(n_chunks), budget / plane)));
 }
 
 int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes& peers,

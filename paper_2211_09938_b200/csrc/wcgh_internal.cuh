@@ -89,6 +89,15 @@ inline bool peers_aligned16(const PeerPlanes& pp) {
   return true;
 }
 
+// Chunks of fixed-order partial sums per launch group (direct K3 and LUT K4).
+// Each group's reduction rounds the running plane to fp32, so the group
+// boundaries are part of the summation order: they are sized from the FULL
+// plane (nh^2), never from the row band, so every band — any GPU count —
+// adds its chunks in the same groups and the gathered plane is bitwise the
+// single-GPU plane. Budget: 2 GiB of fp32 complex partial planes, or
+// WCGH_PARTIAL_BYTES (tests force several groups with a small value).
+int partial_group(int n_chunks, int nh);
+
 // copy a finished band into the peer planes (used where no fused epilogue exists)
 int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes& peers,
                          cudaStream_t stream);

@@ -316,7 +316,6 @@ __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, siz
 }
 
 constexpr int kMaxChunkSteps = 4096;
-constexpr size_t kPartialBytes = 2ull << 30;
 
 // Register-window shape: R rows x PX columns per thread, D rows of prefetch,
 // W warps per CTA. Default 8 x 2 x 2 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
@@ -448,7 +447,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + target - 1) / target));
   chunk_steps = (chunk_steps + 127) / 128 * 128;
   const int n_chunks = (sc.n_dense + chunk_steps - 1) / chunk_steps;
-  const int group = int(std::max<size_t>(1, std::min<size_t>(n_chunks, kPartialBytes / (band * sizeof(float2)))));
+  const int group = partial_group(n_chunks, nh);
   float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
   const int tiles_x = (nh + 32 * v.PX - 1) / (32 * v.PX);
   const int groups = (rows + block * v.R - 1) / (block * v.R);  // per row residue

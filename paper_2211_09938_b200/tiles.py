@@ -76,7 +76,17 @@ class PeerPlaneExchange:
     each rank maps its peers' planes. A job registered with `register` then
     writes its band into every rank's plane from the epilogue of the kernel
     that produces it (wcgh_job_set_peer_planes) — no collective per step; a
-    barrier tells the ranks when all bands have landed."""
+    barrier tells the ranks when all bands have landed.
+
+    The planes are double-buffered with a step epoch: step k stores into
+    buffer k % 2 on every rank, so a rank still reading step k's plane after
+    the barrier (e.g. its D2H copy) is never overwritten by a faster peer
+    already producing step k + 1; step k + 2 reuses the buffer only after
+    every rank has passed step k + 1's barrier, i.e. after its read of step k.
+    Use `run(job)` per step (flip + run) and `plane_tensor()` for the plane of
+    the last step."""
+
+    NBUF = 2
 
     def __init__(self, world: int, rank: int, plane_size: int, device: int):
         import ctypes as C
@@ -87,33 +97,39 @@ class PeerPlaneExchange:
 
         self.lib = L.load()
         self.n, self.world, self.rank, self.device = plane_size, world, rank, device
-        self.own, self.ptrs, self.opened = 0, [], []
+        self.own, self.ptrs, self.opened = [], [[] for _ in range(self.NBUF)], []
+        self.epoch, self.current, self.job = 0, None, None
         # every step is agreed on by all ranks, so a failure on one rank makes
         # all of them raise (and fall back) instead of leaving some blocked
-        handle = None
+        handles_own, err = None, ""
         try:
-            own = C.c_void_p()
-            buf = C.create_string_buffer(64)
-            L.check(self.lib.wcgh_ipc_alloc_plane(device, plane_size, C.byref(own), buf))
-            self.own, handle = int(own.value), buf.raw
+            hs = []
+            for _ in range(self.NBUF):
+                own = C.c_void_p()
+                buf = C.create_string_buffer(64)
+                L.check(self.lib.wcgh_ipc_alloc_plane(device, plane_size, C.byref(own), buf))
+                self.own.append(int(own.value))
+                hs.append(buf.raw)
+            handles_own = hs
         except Exception as e:  # noqa: BLE001
             err = f"rank {rank}: {e}"
         handles = [None] * world
-        dist.all_gather_object(handles, handle)
+        dist.all_gather_object(handles, handles_own)
         if any(h is None for h in handles):
             self.close()
             raise RuntimeError("peer planes: IPC allocation failed on some rank"
-                               + (f" ({err})" if handle is None else ""))
+                               + (f" ({err})" if handles_own is None else ""))
         ok = True
         try:
-            for r, h in enumerate(handles):
-                if r == rank:
-                    self.ptrs.append(self.own)
-                    continue
-                p = C.c_void_p()
-                L.check(self.lib.wcgh_ipc_open_plane(device, h, C.byref(p)))
-                self.ptrs.append(int(p.value))
-                self.opened.append(int(p.value))
+            for b in range(self.NBUF):
+                for r, hs in enumerate(handles):
+                    if r == rank:
+                        self.ptrs[b].append(self.own[b])
+                        continue
+                    p = C.c_void_p()
+                    L.check(self.lib.wcgh_ipc_open_plane(device, hs[b], C.byref(p)))
+                    self.ptrs[b].append(int(p.value))
+                    self.opened.append(int(p.value))
         except Exception as e:  # noqa: BLE001
             ok, err = False, f"rank {rank}: {e}"
         oks = [None] * world
@@ -124,13 +140,26 @@ class PeerPlaneExchange:
                                + (f" ({err})" if not ok else ""))
 
     def register(self, job) -> None:
-        job.set_peer_planes(self.ptrs)
+        self.job = job
+
+    def run(self, job=None) -> None:
+        """One step: point the job's fused gather at this epoch's buffers and
+        run it. The caller's barrier after this marks every band landed."""
+        job = job or self.job
+        b = self.epoch % self.NBUF
+        job.set_peer_planes(self.ptrs[b])
+        job.run()
+        self.current = b
+        self.epoch += 1
 
     def plane_tensor(self):
-        """torch (Nh, 2*Nh) float32 view of this rank's assembled plane."""
+        """torch (Nh, 2*Nh) float32 view of this rank's plane assembled by the
+        last step."""
         import torch
 
-        return torch.as_tensor(CudaView(self.own, (self.n, 2 * self.n)), device="cuda")
+        if self.current is None:
+            raise RuntimeError("peer planes: no step has run")
+        return torch.as_tensor(CudaView(self.own[self.current], (self.n, 2 * self.n)), device="cuda")
 
     def close(self) -> None:
         import ctypes as C
@@ -138,9 +167,9 @@ class PeerPlaneExchange:
         for p in self.opened:
             self.lib.wcgh_ipc_close_plane(C.c_void_p(p))
         self.opened = []
-        if self.own:
-            self.lib.wcgh_ipc_free_plane(C.c_void_p(self.own))
-            self.own = 0
+        for p in self.own:
+            self.lib.wcgh_ipc_free_plane(C.c_void_p(p))
+        self.own = []
 
 
 def as_complex(plane_f32) -> np.ndarray:

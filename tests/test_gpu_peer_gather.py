@@ -8,11 +8,14 @@ another (host barrier only), and on a multi-GPU box the same stores go over
 NVLink (cudaIpcMemLazyEnablePeerAccess)."""
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+FRACS = (0.25, 0.5, 0.1, 1.0, 0.0)
 
 
 def _free_port():
@@ -45,11 +48,24 @@ def _worker(rank, world, port, method, out_dir):
     ex.register(job)
     for _ in range(2):  # twice: the planes are overwritten, not accumulated
         job.upload(sc.objects, sc.masks)
-        job.run()
+        ex.run()
         torch.cuda.synchronize()
         dist.barrier()
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), tiles.as_complex(ex.plane_tensor()))
     np.save(os.path.join(out_dir, f"band{rank}.npy"), job.download())
+    dist.barrier()
+    # new inputs every step, no barrier after the read: rank 0 reads each
+    # step's plane late (after a sleep) while rank 1 already produces the next
+    # step — the double-buffered planes (step epoch) keep rank 0's copy intact
+    for k, frac in enumerate(FRACS):
+        sk = scenes.make_scene(0, saliency_frac=frac)
+        job.upload(sk.objects, sk.masks)
+        ex.run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            time.sleep(0.3)
+        np.save(os.path.join(out_dir, f"step{k}_rank{rank}.npy"), tiles.as_complex(ex.plane_tensor()))
     dist.barrier()
     ex.close()
     job.close()
@@ -73,3 +89,8 @@ def test_two_rank_fused_gather_equals_single_process(ctx, method, tmp_path):
         assert np.array_equal(got, full), (method, r)
         band = np.load(tmp_path / f"band{r}.npy")
         assert np.array_equal(band, full[r * 64:(r + 1) * 64])
+    for k, frac in enumerate(FRACS):
+        sk = scenes.make_scene(0, saliency_frac=frac)
+        ref = HologramJob(spec_for_scene(sk, method=method))(sk.objects, sk.masks)
+        for r in range(world):
+            assert np.array_equal(np.load(tmp_path / f"step{k}_rank{r}.npy"), ref), (method, k, r)
