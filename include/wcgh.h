@@ -204,6 +204,51 @@ int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, 
                 const double* d, int m, const double* saliency_finer, double threshold,
                 float* plane, uint8_t* mask_out, uint64_t* ops_out);
 
+/* ---- device-resident LUTs and planes (the caller's FringeLut / ComplexField)
+ * The reference's apply_block / synthesize_base / refine read the CALLER's
+ * FringeLut samples (lut.support(), synthesis.cpp:18-42,149-178), which may
+ * come from the f32 CGHL cache (pipeline.cpp:174-177) or be built by the
+ * caller. A wcgh_lut holds such a support on the device (uploaded once, in a
+ * guarded allocation the superposition kernel reads without bounds checks);
+ * a wcgh_plane is a device-resident n x n complex64 hologram that stage
+ * calls accumulate into with no host round trip. */
+typedef struct wcgh_lut wcgh_lut;
+typedef struct wcgh_plane wcgh_plane;
+/* FringeLut(scene, block, support) (fringe_lut.cpp:34-51) on the device:
+ * `samples` = the (2n-1)^2 support, row-major, interleaved (re, im) as
+ * complex64 (dtype WCGH_F32, the CGHL payload) or complex128 (WCGH_F64, the
+ * reference's std::complex<double>; rounded once to complex64), or NULL to
+ * build it on the device (build_block_lut, fringe_lut.cpp:53-93). Non-finite
+ * samples are a ValidationError. */
+int wcgh_lut_create(wcgh_ctx* ctx, const wcgh_layer* scene, int n, int block, const void* samples,
+                    int dtype, wcgh_lut** out);
+void wcgh_lut_destroy(wcgh_lut* lut);
+/* D2H of the device support (complex64 (2n-1)^2). */
+int wcgh_lut_download(wcgh_lut* lut, float* out);
+/* An n x n complex64 plane on the context's device, zeroed. */
+int wcgh_plane_create(wcgh_ctx* ctx, int n, wcgh_plane** out);
+void wcgh_plane_destroy(wcgh_plane* plane);
+int wcgh_plane_zero(wcgh_plane* plane);
+/* H2D / D2H of the whole plane, complex64 (WCGH_F32) or complex128 (WCGH_F64). */
+int wcgh_plane_upload(wcgh_plane* plane, const void* host, int dtype);
+int wcgh_plane_download(wcgh_plane* plane, void* host, int dtype);
+/* Device pointer of the plane (n*n complex64), e.g. for a zero-copy view. */
+void* wcgh_plane_dev(wcgh_plane* plane);
+/* apply_block (synthesis.cpp:149-160) batched, with the caller's LUT:
+ * plane += sum_i (w_re[i] + i w_im[i]) * crop(S_B at cell_i); cells y*m+x
+ * on the m = n/B grid (out of range: ValidationError); w_im may be NULL;
+ * ops_out += n_cells (zero weights count, synthesis.cpp:20). */
+int wcgh_lut_apply_blocks(wcgh_lut* lut, const uint32_t* cells, const float* w_re,
+                          const float* w_im, int64_t n_cells, wcgh_plane* plane,
+                          uint64_t* ops_out);
+/* refine (synthesis.cpp:171-178 + 90-123) with the caller's LUT: residual of
+ * (h, v, d) (m x m doubles), strict '>' gate against saliency_finer (2m x 2m
+ * doubles), plane += the gated cells' superposition; B = n / (2m) must be
+ * the LUT's block size. mask_out (2m x 2m) may be NULL. */
+int wcgh_lut_refine(wcgh_lut* lut, const double* h, const double* v, const double* d, int m,
+                    const double* saliency_finer, double threshold, wcgh_plane* plane,
+                    uint8_t* mask_out, uint64_t* ops_out);
+
 /* ---- jobs: resident inputs, device-side hologram ------------------------ */
 int wcgh_job_create(wcgh_ctx* ctx, const wcgh_desc* desc, wcgh_job** out);
 void wcgh_job_destroy(wcgh_job* job);
@@ -317,6 +362,12 @@ int wcgh_read_cghl(const char* path, float* lut, int64_t capacity, int* n_out, i
  * creation) with caller data, (2N-1)^2 complex64 — e.g. a reference CGHL
  * cache, so the job superposes exactly the reference's LUT samples. */
 int wcgh_job_load_lut(wcgh_job* job, int layer, int block, const float* lut);
+/* The same from a device LUT (wcgh_lut_create; device-to-device): the LUT
+ * job of synthesize_progressive(..., const LutSet& luts, ...) superposes the
+ * caller's LutSet (synthesis.cpp:180-253 reads luts.of(B)). The LUT's plane
+ * size must equal the job's; its scene must equal the layer's (the
+ * reference's "LUTs built for a different scene" check). */
+int wcgh_job_use_lut(wcgh_job* job, int layer, const wcgh_lut* lut);
 
 /* One-shot: job create + upload + run + download + destroy. The entry the
  * C++ synthesize_progressive mirror calls (synthesis.hpp:88-91). */

@@ -321,6 +321,40 @@ def ref_build_block_lut(wl, pitch, z, n, block, workers=0):
     return out
 
 
+def ref_apply_block_lut(plane, support, wl, pitch, z, block, cx, cy, w):
+    """apply_block (synthesis.cpp:149-160) of the reference with the CALLER's
+    LUT samples (FringeLut(scene, block, support)); plane complex128, returned
+    updated, plus the op count."""
+    p = np.ascontiguousarray(plane, np.complex128).copy()
+    sup = np.ascontiguousarray(support, np.complex128)
+    n = p.shape[0]
+    ops = C.c_uint64()
+    w = complex(w)
+    _ref_check(ref().ref_apply_block_lut(C.c_double(wl), C.c_double(pitch), C.c_double(z), C.c_int(n),
+                                         C.c_int(block), _p(sup), C.c_int(cx), C.c_int(cy),
+                                         C.c_double(w.real), C.c_double(w.imag), _p(p), C.byref(ops)))
+    return p, int(ops.value)
+
+
+def ref_synthesize_progressive_luts(obj, sal, wl, pitch, z, supports, t=(0.5, 0.7, 0.9),
+                                    en=(1, 1, 1)):
+    """synthesize_progressive with a caller LutSet; supports = {1: S1, 2: S2,
+    4: S4, 8: S8}, (2n-1)^2 complex128 each. Returns (planes[4], ops[5])."""
+    obj = np.ascontiguousarray(obj, np.float64)
+    sal = np.ascontiguousarray(sal, np.float64)
+    n = obj.shape[0]
+    sups = [np.ascontiguousarray(supports[b], np.complex128) for b in (1, 2, 4, 8)]
+    arr = (C.c_void_p * 4)(*[a.ctypes.data for a in sups])
+    planes = np.empty((4, n, n), np.complex128)
+    ops = np.zeros(5, np.uint64)
+    th = np.array(t, np.float64)
+    ens = np.array(en, np.int32)
+    _ref_check(ref().ref_synthesize_progressive_luts(
+        _p(obj), _p(sal), C.c_int(n), C.c_double(wl), C.c_double(pitch), C.c_double(z), _p(th),
+        _p(ens), arr, _p(planes), _p(ops)))
+    return planes, ops
+
+
 def ref_synthesize_progressive(obj, sal, wl, pitch, z, t=(0.5, 0.7, 0.9), en=(1, 1, 1),
                                workers=0, seed=None):
     obj = np.ascontiguousarray(obj, np.float64)

@@ -60,6 +60,13 @@ void real_out(const RealImage& im, double* out) {
   std::memcpy(out, im.data().data(), im.size() * sizeof(double));
 }
 
+ComplexField support_in(const double* p, std::size_t span) {
+  const int w = static_cast<int>(span);
+  ComplexField f(w, w);
+  std::memcpy(f.data().data(), p, span * span * sizeof(std::complex<double>));
+  return f;
+}
+
 RefinementPlan plan_of(const double* t, const int* en) {
   RefinementPlan plan;
   plan.t_ll = t[0];
@@ -154,6 +161,45 @@ int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx,
     apply_block(p, lut, GridCell{cx, cy}, {w_re, w_im}, counter, OpLevel::kRefineFull);
     complex_out(p, plane);
     *ops = counter.get(OpLevel::kRefineFull);
+  });
+}
+
+// apply_block with the CALLER's LUT samples: FringeLut(scene, block, support)
+// (fringe_lut.cpp:34-51) from a (2n-1)^2 complex<double> array.
+int ref_apply_block_lut(double wl, double pitch, double z, int n, int block,
+                        const double* support, int cx, int cy, double w_re, double w_im,
+                        double* plane, std::uint64_t* ops) {
+  return guard([&] {
+    const SceneParams scene = make_scene(wl, pitch, z, n);
+    const std::size_t span = std::size_t(2 * n - 1);
+    const FringeLut lut(scene, block, support_in(support, span));
+    ComplexField p(n, n);
+    std::memcpy(p.data().data(), plane, p.size() * sizeof(std::complex<double>));
+    OpCounter counter;
+    apply_block(p, lut, GridCell{cx, cy}, {w_re, w_im}, counter, OpLevel::kRefineFull);
+    complex_out(p, plane);
+    *ops = counter.get(OpLevel::kRefineFull);
+  });
+}
+
+// synthesize_progressive with a CALLER LutSet: supports[k] = the (2n-1)^2
+// complex<double> samples of block 1, 2, 4, 8 (k = 0..3).
+int ref_synthesize_progressive_luts(const double* object, const double* saliency, int n,
+                                    double wl, double pitch, double z, const double* thresholds,
+                                    const int* enables, const double* const* supports,
+                                    double* planes_out, std::uint64_t* ops_out) {
+  return guard([&] {
+    const SceneParams scene = make_scene(wl, pitch, z, n);
+    const std::size_t span = std::size_t(2 * n - 1);
+    LutSet luts;
+    const int blocks[4] = {1, 2, 4, 8};
+    for (int k = 0; k < 4; ++k) {
+      luts.put(FringeLut(scene, blocks[k], support_in(supports[k], span)));
+    }
+    const ProgressiveResult r = synthesize_progressive(real_in(object, n), real_in(saliency, n), scene,
+                                                       plan_of(thresholds, enables), luts, 0);
+    for (int i = 0; i < 4; ++i) complex_out(r.stage(i), planes_out + 2 * std::size_t(i) * n * n);
+    for (int i = 0; i < kOpLevelCount; ++i) ops_out[i] = r.ops.get(kAllOpLevels[i]);
   });
 }
 

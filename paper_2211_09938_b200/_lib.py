@@ -112,6 +112,20 @@ _SIGS = [
     ("wcgh_read_cghl", C.c_int, [C.c_char_p, _VP, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                  C.POINTER(Layer)]),
     ("wcgh_job_load_lut", C.c_int, [_VP, C.c_int, C.c_int, _VP]),
+    ("wcgh_job_use_lut", C.c_int, [_VP, C.c_int, _VP]),
+    ("wcgh_lut_create", C.c_int, [_VP, C.POINTER(Layer), C.c_int, C.c_int, _VP, C.c_int,
+                                  C.POINTER(_VP)]),
+    ("wcgh_lut_destroy", None, [_VP]),
+    ("wcgh_lut_download", C.c_int, [_VP, _VP]),
+    ("wcgh_plane_create", C.c_int, [_VP, C.c_int, C.POINTER(_VP)]),
+    ("wcgh_plane_destroy", None, [_VP]),
+    ("wcgh_plane_zero", C.c_int, [_VP]),
+    ("wcgh_plane_upload", C.c_int, [_VP, _VP, C.c_int]),
+    ("wcgh_plane_download", C.c_int, [_VP, _VP, C.c_int]),
+    ("wcgh_plane_dev", _VP, [_VP]),
+    ("wcgh_lut_apply_blocks", C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, _VP, C.POINTER(C.c_uint64)]),
+    ("wcgh_lut_refine", C.c_int, [_VP, _VP, _VP, _VP, C.c_int, _VP, C.c_double, _VP, _VP,
+                                  C.POINTER(C.c_uint64)]),
     ("wcgh_synthesize", C.c_int, [_VP, C.POINTER(Desc), _VP, _VP, _VP, C.POINTER(Stats)]),
     ("wcgh_synthesize_multi", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(Desc), _VP, _VP, _VP,
                                         C.POINTER(Stats)]),

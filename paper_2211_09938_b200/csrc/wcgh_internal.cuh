@@ -351,6 +351,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
 // superposes.
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,
                      int row0, int rows, float2* out, StageCells& sc, DevBuf& partial,
-                     cudaStream_t stream, long long* nnz_out);
+                     cudaStream_t stream, long long* nnz_out, bool accumulate = false,
+                     bool rotate = false);
 
 }  // namespace wcgh

@@ -476,7 +476,7 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
 
 int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m, int off,
                      int row0, int rows, float2* out, StageCells& sc, DevBuf& partial,
-                     cudaStream_t s, long long* nnz_out) {
+                     cudaStream_t s, long long* nnz_out, bool accumulate, bool rotate) {
   int launches = launch_stage_cells(w, m, sc, s);
   int tot[3];
   stage_cells_totals_async(sc, tot, s);
@@ -486,7 +486,7 @@ int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m
   sc.nnz = tot[2];
   if (nnz_out) *nnz_out = sc.nnz;
   return launches + launch_lut_stage(lut, nh, block, sc, off, row0, rows, out, partial, s, nullptr,
-                                    false);
+                                    accumulate || rotate, rotate);
 }
 
 }  // namespace wcgh

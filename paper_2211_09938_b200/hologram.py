@@ -163,6 +163,11 @@ class HologramJob:
         lut = np.ascontiguousarray(lut, np.complex64)
         L.check(self.ctx.lib.wcgh_job_load_lut(self.h, int(layer), int(block), L.ptr(lut)))
 
+    def use_lut(self, layer: int, lut) -> None:
+        """LUT method: superpose a device LUT (stages.DeviceLut — e.g. the
+        caller's FringeLut samples) for `layer` at its block size."""
+        L.check(self.ctx.lib.wcgh_job_use_lut(self.h, int(layer), lut.h))
+
     def set_peer_planes(self, ptrs) -> None:
         """Fused row-tile gather: device pointers of full planes (this rank's and
         the IPC-mapped peers') that every run also writes its band into."""

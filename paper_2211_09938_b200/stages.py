@@ -154,6 +154,116 @@ def refine(plane: np.ndarray, layer, h, v, d, saliency_finer, threshold: float, 
     return mask, int(ops.value)
 
 
+_CPLX = {np.dtype(np.complex64): L.F32, np.dtype(np.complex128): L.F64}
+
+
+class DevicePlane:
+    """wcgh_plane: an n x n complex64 hologram resident on the device; stage
+    calls (DeviceLut.apply_blocks / refine) accumulate into it with no host
+    round trip."""
+
+    def __init__(self, n: int, ctx=None):
+        self.ctx = _ctx(ctx)
+        self.n = int(n)
+        h = C.c_void_p()
+        L.check(self.ctx.lib.wcgh_plane_create(self.ctx.h, self.n, C.byref(h)))
+        self.h = h
+
+    def zero(self) -> "DevicePlane":
+        L.check(self.ctx.lib.wcgh_plane_zero(self.h))
+        return self
+
+    def upload(self, plane: np.ndarray) -> "DevicePlane":
+        a = np.ascontiguousarray(plane)
+        if a.shape != (self.n, self.n) or a.dtype not in _CPLX:
+            raise L.ValidationError("plane_upload: need an n x n complex64/complex128 array")
+        L.check(self.ctx.lib.wcgh_plane_upload(self.h, L.ptr(a), _CPLX[a.dtype]))
+        return self
+
+    def download(self, dtype=np.complex64) -> np.ndarray:
+        out = np.empty((self.n, self.n), dtype)
+        L.check(self.ctx.lib.wcgh_plane_download(self.h, L.ptr(out), _CPLX[np.dtype(dtype)]))
+        return out
+
+    def dev_ptr(self) -> int:
+        return int(self.ctx.lib.wcgh_plane_dev(self.h) or 0)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.wcgh_plane_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceLut:
+    """wcgh_lut: a block LUT S_B resident on the device — the caller's samples
+    (a FringeLut's support, complex64 or complex128) uploaded once, or built
+    on the device when samples is None."""
+
+    def __init__(self, layer, n: int, block: int, samples: np.ndarray | None = None, ctx=None):
+        self.ctx = _ctx(ctx)
+        self.layer, self.n, self.block = tuple(layer), int(n), int(block)
+        lay = L.Layer(*layer)
+        if samples is None:
+            sp, dt = None, L.F32
+        else:
+            a = np.ascontiguousarray(samples)
+            span = 2 * self.n - 1
+            if a.shape != (span, span) or a.dtype not in _CPLX:
+                raise L.ValidationError("FringeLut: support must be (2N-1) x (2N-1) complex")
+            sp, dt = L.ptr(a), _CPLX[a.dtype]
+        h = C.c_void_p()
+        L.check(self.ctx.lib.wcgh_lut_create(self.ctx.h, C.byref(lay), self.n, self.block, sp, dt,
+                                             C.byref(h)))
+        self.h = h
+
+    def download(self) -> np.ndarray:
+        span = 2 * self.n - 1
+        out = np.empty((span, span), np.complex64)
+        L.check(self.ctx.lib.wcgh_lut_download(self.h, L.ptr(out)))
+        return out
+
+    def apply_blocks(self, plane: DevicePlane, cells, w_re, w_im=None) -> int:
+        """plane += sum_i (w_re + i w_im)_i crop(S_B at cell_i); returns ops."""
+        cells = np.ascontiguousarray(cells, np.uint32)
+        wr = np.ascontiguousarray(w_re, np.float32)
+        wi = None if w_im is None else np.ascontiguousarray(w_im, np.float32)
+        ops = C.c_uint64(0)
+        L.check(self.ctx.lib.wcgh_lut_apply_blocks(self.h, L.ptr(cells), L.ptr(wr), L.ptr(wi),
+                                                   len(cells), plane.h, C.byref(ops)))
+        return int(ops.value)
+
+    def refine(self, plane: DevicePlane, h, v, d, saliency_finer, threshold: float):
+        h, v, d = (np.ascontiguousarray(a, np.float64) for a in (h, v, d))
+        sal = np.ascontiguousarray(saliency_finer, np.float64)
+        m = h.shape[0]
+        if v.shape != h.shape or d.shape != h.shape:
+            raise L.ValidationError("expand_residual: detail subbands differ in size")
+        if sal.shape != (2 * m, 2 * m):
+            raise L.ValidationError("refine: saliency level does not match the residual resolution")
+        mask = np.empty((2 * m, 2 * m), np.uint8)
+        ops = C.c_uint64(0)
+        L.check(self.ctx.lib.wcgh_lut_refine(self.h, L.ptr(h), L.ptr(v), L.ptr(d), m, L.ptr(sal),
+                                             float(threshold), plane.h, L.ptr(mask), C.byref(ops)))
+        return mask, int(ops.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.wcgh_lut_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def write_cgh1(path, plane: np.ndarray, layer) -> None:
     """save_hologram (image_io.cpp:220-242): CGH1 header + f32 (re, im) payload."""
     plane = np.ascontiguousarray(plane, np.complex64)

@@ -267,13 +267,29 @@ class FringeLut:
     """fringe_lut.hpp:45-62: (2N-1)^2 support of a B x B block (complex64,
     the CGHL payload precision)."""
 
-    def __init__(self, scene: SceneParams, block_size: int, support: np.ndarray):
+    def __init__(self, scene: SceneParams, block_size: int, support: np.ndarray, _owned=False):
         if block_size not in LUT_BLOCK_SIZES:
             raise ValidationError(f"FringeLut: unsupported block size {block_size}")
         span = 2 * scene.plane_size() - 1
         if support.shape != (span, span):
             raise ValidationError("FringeLut: support must be (2N-1) x (2N-1)")
-        self._scene, self._b, self._support = scene, block_size, support
+        # the reference's FringeLut owns its samples (value semantics,
+        # fringe_lut.cpp:34-51): keep a private read-only copy, so the device
+        # copy made once by device() can never go stale
+        sup = support if _owned else np.array(support, copy=True)
+        sup.setflags(write=False)
+        self._scene, self._b, self._support = scene, block_size, sup
+        self._dev = None
+
+    def device(self) -> "stages.DeviceLut":
+        """These samples on the device (uploaded on first use): what every
+        apply_block / refine / synthesize_* call superposes, as the
+        reference's apply_block_unchecked reads lut.support()
+        (synthesis.cpp:18-42)."""
+        if self._dev is None:
+            self._dev = stages.DeviceLut(self._scene.layer(), self._scene.plane_size(), self._b,
+                                         self._support)
+        return self._dev
 
     def scene(self) -> SceneParams:
         return self._scene
@@ -298,7 +314,7 @@ def build_block_lut(scene: SceneParams, block_size: int, workers: int = 1) -> Fr
     if block_size > scene.plane_size():
         raise ValidationError("build_block_lut: block size exceeds plane size")
     sup = stages.build_block_lut(scene.layer(), scene.plane_size(), block_size)
-    return FringeLut(scene, block_size, sup)
+    return FringeLut(scene, block_size, sup, _owned=True)
 
 
 def lut_cache_store(lut: FringeLut, path) -> None:
@@ -315,7 +331,7 @@ def lut_cache_load(path, expected_scene: SceneParams, expected_block_size: int) 
         raise StaleCacheError(f"lut cache: block size {block} != expected {expected_block_size}")
     if n != expected_scene.plane_size() or tuple(layer) != tuple(expected_scene.layer()):
         raise StaleCacheError(f"lut cache: scene parameters in {path} do not match the requested scene")
-    return FringeLut(expected_scene, expected_block_size, support)
+    return FringeLut(expected_scene, expected_block_size, support, _owned=True)
 
 
 class LutSet:
@@ -406,9 +422,24 @@ class ProgressiveResult:
         return [self.base_lll, self.after_ll, self.after_l, self.after_full][index]
 
 
-def _plane_matches(plane: np.ndarray, lut: FringeLut, where: str) -> int:
+DevicePlane = stages.DevicePlane  # a device-resident ComplexField
+
+_scratch: dict = {}
+
+
+def _scratch_plane(n: int) -> "stages.DevicePlane":
+    """Per-size device plane for calls on host (numpy) planes: the
+    contribution is formed on the device, then added on the host."""
+    p = _scratch.get(n)
+    if p is None:
+        p = _scratch[n] = stages.DevicePlane(n)
+    return p.zero()
+
+
+def _plane_matches(plane, lut: FringeLut, where: str) -> int:
     n = lut.scene().plane_size()
-    if plane.shape != (n, n):
+    shape = (plane.n, plane.n) if isinstance(plane, stages.DevicePlane) else plane.shape
+    if shape != (n, n):
         raise ValidationError(f"{where}: plane size does not match the LUT scene")
     return n
 
@@ -417,9 +448,11 @@ def _add_contribution(plane: np.ndarray, contrib: np.ndarray) -> None:
     plane += contrib.astype(plane.dtype, copy=False)
 
 
-def apply_block(plane: np.ndarray, lut: FringeLut, cell: GridCell, weight: complex,
+def apply_block(plane, lut: FringeLut, cell: GridCell, weight: complex,
                 counter: OpCounter, level: OpLevel) -> None:
-    """synthesis.cpp:149-160: plane += weight * crop(S_B at cell * B), in place."""
+    """synthesis.cpp:149-160: plane += weight * crop(S_B at cell * B), in place,
+    with the caller's LUT samples. `plane` is a numpy ComplexField (the
+    contribution is added on the host) or a DevicePlane (stays on the device)."""
     n = _plane_matches(plane, lut, "apply_block")
     b = lut.block_size()
     cells = n // b
@@ -427,18 +460,17 @@ def apply_block(plane: np.ndarray, lut: FringeLut, cell: GridCell, weight: compl
         raise ValidationError(f"apply_block: cell ({cell.x},{cell.y}) out of range")
     w = complex(weight)
     idx = [cell.y * cells + cell.x]
-    for part, val in ((0, w.real), (1, w.imag)):
-        if val == 0.0:
-            continue
-        c = np.zeros((n, n), np.complex64)
-        stages.apply_blocks(c, lut.scene().layer(), b, idx, [val])
-        _add_contribution(plane, c if part == 0 else 1j * c.astype(np.complex128))
+    target = plane if isinstance(plane, stages.DevicePlane) else _scratch_plane(n)
+    lut.device().apply_blocks(target, idx, [w.real], [w.imag] if w.imag != 0.0 else None)
+    if target is not plane:
+        _add_contribution(plane, target.download(np.complex128))
     counter.add(level, 1)
 
 
 def synthesize_base(pyramid: HaarPyramid, saliency: SaliencyPyramid, luts: LutSet,
                     counter: OpCounter, workers: int = 1) -> np.ndarray:
-    """synthesis.cpp:162-169 / 77-88: the B = 8 LUT on every approximation cell."""
+    """synthesis.cpp:162-169 / 77-88: the caller's B = 8 LUT on every
+    approximation cell."""
     if saliency.full_size() != pyramid.original_size:
         raise ValidationError("synthesize_base: saliency and pyramid sizes differ")
     block = pyramid.original_size // pyramid.approx.shape[0]
@@ -447,17 +479,17 @@ def synthesize_base(pyramid: HaarPyramid, saliency: SaliencyPyramid, luts: LutSe
     m = pyramid.approx.shape[0]
     if m * block != n:
         raise ValidationError("synthesize_base: approximation grid does not tile the plane")
-    plane = np.zeros((n, n), np.complex64)
-    ops = stages.apply_blocks(plane, lut.scene().layer(), block, np.arange(m * m),
-                              pyramid.approx.ravel())
+    plane = _scratch_plane(n)
+    ops = lut.device().apply_blocks(plane, np.arange(m * m), pyramid.approx.ravel())
     counter.add(OpLevel.BASE_LLL, ops)
-    return plane.astype(np.complex128)
+    return plane.download(np.complex128)
 
 
-def refine(plane: np.ndarray, detail_h, detail_v, detail_d, saliency_finer, lut: FringeLut,
+def refine(plane, detail_h, detail_v, detail_d, saliency_finer, lut: FringeLut,
            threshold: float, counter: OpCounter, level: OpLevel, mask: GateMask | None = None,
            workers: int = 1) -> None:
-    """synthesis.cpp:171-178 + 90-123: residual, strict '>' gate, block LUT."""
+    """synthesis.cpp:171-178 + 90-123: residual, strict '>' gate, the caller's
+    block LUT; numpy plane (host add) or DevicePlane (on the device)."""
     n = _plane_matches(plane, lut, "refine")
     h, v, d = (np.asarray(a, np.float64) for a in (detail_h, detail_v, detail_d))
     if not (h.shape == v.shape == d.shape):
@@ -468,9 +500,10 @@ def refine(plane: np.ndarray, detail_h, detail_v, detail_d, saliency_finer, lut:
         raise ValidationError("refine: saliency level does not match the residual resolution")
     if 2 * m * lut.block_size() != n:
         raise ValidationError("refine: LUT block size does not match the residual level")
-    c = np.zeros((n, n), np.complex64)
-    on, ops = stages.refine(c, lut.scene().layer(), h, v, d, sal, threshold)
-    _add_contribution(plane, c)
+    target = plane if isinstance(plane, stages.DevicePlane) else _scratch_plane(n)
+    on, ops = lut.device().refine(target, h, v, d, sal, threshold)
+    if target is not plane:
+        _add_contribution(plane, target.download(np.complex128))
     counter.add(level, ops)
     if mask is not None:
         mask.width = mask.height = 2 * m
@@ -519,6 +552,9 @@ def synthesize_progressive(object_: np.ndarray, saliency: np.ndarray, scene: Sce
     src = obj if random_phase_seed is None else random_phase_field(obj, random_phase_seed)
     job = _job(n, scene, plan, method, "f64" if random_phase_seed is None else "c128")
     try:
+        if method == "lut":  # the caller's LutSet (synthesis.cpp:230-250 reads luts.of(B))
+            for b in LUT_BLOCK_SIZES:
+                job.use_lut(0, luts.of(b).device())
         job(np.ascontiguousarray(src), np.ascontiguousarray(sal))
         st = job.stats()
         snaps = job.download_stages()
@@ -552,20 +588,18 @@ def synthesize_pointwise_oracle(object_: np.ndarray, scene: SceneParams, counter
     if not (unit_lut.scene() == scene):
         raise ValidationError("pointwise oracle: LUT built for a different scene")
     _require_finite(obj, "object")
-    plane = np.zeros((n, n), np.complex64)
+    plane = _scratch_plane(n)
     cells = np.arange(n * n)
     if random_phase_seed is None:
-        ops = stages.apply_blocks(plane, scene.layer(), 1, cells, obj.ravel())
-        counter.add(OpLevel.POINTWISE_ORACLE, ops)
-        return plane.astype(np.complex128)
-    # complex amplitudes (synthesis.cpp:269-284): real and imaginary weights
-    # superposed separately, combined by linearity; one operator per cell
-    rotated = random_phase_field(obj, random_phase_seed)
-    ops = stages.apply_blocks(plane, scene.layer(), 1, cells, rotated.real.ravel())
-    plane_im = np.zeros((n, n), np.complex64)
-    stages.apply_blocks(plane_im, scene.layer(), 1, cells, rotated.imag.ravel())
+        ops = unit_lut.device().apply_blocks(plane, cells, obj.ravel())
+    else:
+        # complex amplitudes (synthesis.cpp:269-284): plane += (re + i im) S_1;
+        # one operator per cell
+        rotated = random_phase_field(obj, random_phase_seed)
+        ops = unit_lut.device().apply_blocks(plane, cells, rotated.real.ravel(),
+                                             rotated.imag.ravel())
     counter.add(OpLevel.POINTWISE_ORACLE, ops)
-    return plane.astype(np.complex128) + 1j * plane_im.astype(np.complex128)
+    return plane.download(np.complex128)
 
 
 # ---- fft.hpp / angular_spectrum.hpp / metrics.hpp (validation, on the device) ----
