@@ -33,6 +33,12 @@ int ref_reconstruct(const double* holo, int n, double wl, double pitch, double z
                     double* out);
 int ref_apply_block(double wl, double pitch, double z, int n, int block, int cx, int cy,
                     double w_re, double w_im, double* plane, std::uint64_t* ops);
+int ref_apply_block_lut(double wl, double pitch, double z, int n, int block, const double* support,
+                        int cx, int cy, double w_re, double w_im, double* plane, std::uint64_t* ops);
+int ref_synthesize_progressive_luts(const double* object, const double* saliency, int n, double wl,
+                                    double pitch, double z, const double* thresholds,
+                                    const int* enables, const double* const* supports,
+                                    double* planes_out, std::uint64_t* ops_out);
 }
 
 using namespace wavecgh;
@@ -148,6 +154,57 @@ int main() {
     ref_apply_block(wl, pitch, z, n, 2, 1, 2, 0.3, -0.7, pl.data(), &aops);
     EXPECT(rel_l2(plane, pl.data()) <= 1e-5, "apply_block complex weight n=%d", n);
     EXPECT(ac.get(OpLevel::kRefineL) == 1, "apply_block count");
+
+    // the CALLER's LUT samples are what the GPU superposes (synthesis.cpp:
+    // 18-42 reads lut.support()): one perturbed sample of a caller-built
+    // FringeLut moves exactly one pixel by w * delta, as in the reference
+    {
+      const int span = 2 * n - 1;
+      ComplexField sup = luts.of(2).support();
+      const int dx = 3, dy = -2, cx = 1, cy = 2;
+      const std::complex<double> delta(0.37, -0.21), w(0.8, 0.25);
+      sup.at(dx + n - 1, dy + n - 1) += delta;
+      const FringeLut pert(scene, 2, sup);
+      ComplexField p0(n, n), p1(n, n);
+      OpCounter oc;
+      apply_block(p0, luts.of(2), GridCell{cx, cy}, w, oc, OpLevel::kRefineL);
+      apply_block(p1, pert, GridCell{cx, cy}, w, oc, OpLevel::kRefineL);
+      std::vector<double> r1(std::size_t(2) * n * n, 0.0);
+      std::uint64_t o1 = 0;
+      ref_apply_block_lut(wl, pitch, z, n, 2, reinterpret_cast<const double*>(sup.data().data()), cx, cy,
+                          w.real(), w.imag(), r1.data(), &o1);
+      EXPECT(rel_l2(p1, r1.data()) <= 1e-5, "apply_block with a caller-modified LUT n=%d", n);
+      int moved = 0;
+      for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x)
+          if (p1.at(x, y) != p0.at(x, y)) {
+            ++moved;
+            EXPECT(x == cx * 2 + dx && y == cy * 2 + dy, "perturbed LUT moved pixel (%d,%d)", x, y);
+            // complex64 device samples: each plane rounded at the sample's magnitude
+            EXPECT(std::abs(p1.at(x, y) - p0.at(x, y) - w * delta) <=
+                       4e-7 * std::abs(w) * std::abs(sup.at(dx + n - 1, dy + n - 1)) + 1e-7,
+                   "perturbed LUT delta n=%d", n);
+          }
+      EXPECT(moved == 1, "perturbed LUT sample must move exactly one pixel (moved %d)", moved);
+      (void)span;
+      // synthesize_progressive with a caller LutSet whose B=1 LUT is modified
+      LutSet mod = luts;
+      ComplexField s1 = luts.of(1).support();
+      s1.at(n - 1, n - 1) += std::complex<double>(0.05, 0.02);
+      mod.put(FringeLut(scene, 1, s1));
+      const ProgressiveResult rm = synthesize_progressive(object, saliency, scene, plan, mod);
+      std::vector<const double*> sp;
+      for (int b : {1, 2, 4, 8}) sp.push_back(reinterpret_cast<const double*>(mod.of(b).support().data().data()));
+      const double th[3] = {plan.t_ll, plan.t_l, plan.t_full};
+      const int en[3] = {1, 1, 1};
+      std::vector<double> rp(std::size_t(8) * n * n);
+      std::uint64_t rops[5] = {};
+      ref_synthesize_progressive_luts(object.data().data(), saliency.data().data(), n, wl, pitch, z, th, en,
+                                      sp.data(), rp.data(), rops);
+      for (int st = 0; st < 4; ++st)
+        EXPECT(rel_l2(rm.stage(st), rp.data() + std::size_t(2) * st * n * n) <= 1e-5,
+               "synthesize_progressive with a caller-modified LutSet stage %d n=%d", st, n);
+    }
   }
   // fringe_lut.cpp on the device: build_block_lut vs the reference's fp64 LUT
   // (complex64 precision), CGHL round trip through the reference's format

@@ -19,6 +19,12 @@
 //    object is then analysed and synthesised part by part on the device
 //    (WCGH_C128 jobs; the direct method folds the phase into its fixed-point
 //    phase, the LUT method superposes i * the imaginary weights);
+//  * apply_block / synthesize_base / refine / synthesize_pointwise_oracle /
+//    synthesize_progressive(..., luts, ...) superpose the CALLER's FringeLut
+//    samples: each support is uploaded once to a device LUT (wcgh_lut,
+//    rounded to complex64) and cached by address + a hash of all samples;
+//    calls on a host ComplexField form the stage's contribution in a device
+//    plane (wcgh_plane) and add it into the caller's plane on the host;
 //  * build_block_lut runs on the device (K5: fp64 sums, complex64 store — the
 //    CGHL payload precision) and is widened to the FringeLut's
 //    complex<double>; lut_cache_store/load go through the ABI's CGHL I/O;
@@ -29,7 +35,9 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdint>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <optional>
 #include <string>
@@ -72,13 +80,93 @@ ComplexField widen(const std::vector<float>& c, int n) {
   return f;
 }
 
-void add_into(ComplexField& plane, const std::vector<float>& c) {
-  for (std::size_t i = 0; i < plane.size(); ++i)
-    plane.data()[i] += std::complex<double>(double(c[2 * i]), double(c[2 * i + 1]));
-}
-
 RealImage from_flat(const double* p, int n) {
   return RealImage(n, n, std::vector<double>(p, p + std::size_t(n) * n));
+}
+
+// ---- the caller's FringeLuts on the device -------------------------------------
+// apply_block_unchecked reads lut.support() (synthesis.cpp:18-42): the GPU
+// must superpose exactly the caller's samples (built, CGHL-cached or
+// modified). Each FringeLut's support is uploaded once (wcgh_lut_create,
+// complex128 -> complex64 on the device) and cached by the support's address,
+// validated on every use by a hash of ALL its samples, so a different
+// FringeLut at a recycled address is uploaded again. At most kMaxLuts device
+// LUTs are kept (oldest evicted first).
+constexpr std::size_t kMaxLuts = 8;
+struct LutEntry {
+  std::size_t count = 0;
+  wcgh_layer scene{};
+  int block = 0;
+  std::uint64_t hash = 0, stamp = 0;
+  wcgh_lut* h = nullptr;
+};
+std::mutex g_lut_mu;
+std::map<const void*, LutEntry> g_luts;
+std::uint64_t g_stamp = 0;
+
+std::uint64_t hash_samples(const std::complex<double>* p, std::size_t count) {
+  const auto* w = reinterpret_cast<const std::uint64_t*>(p);
+  std::uint64_t h = 1469598103934665603ull;
+  for (std::size_t i = 0; i < 2 * count; ++i) h = (h ^ w[i]) * 1099511628211ull;
+  return h;
+}
+
+wcgh_lut* device_lut(const FringeLut& lut) {
+  const auto& sup = lut.support().data();
+  const void* key = sup.data();
+  const std::uint64_t hash = hash_samples(sup.data(), sup.size());
+  const wcgh_layer L = layer_of(lut.scene());
+  std::lock_guard<std::mutex> lk(g_lut_mu);
+  auto it = g_luts.find(key);
+  if (it != g_luts.end()) {
+    LutEntry& e = it->second;
+    if (e.count == sup.size() && e.block == lut.block_size() && e.hash == hash &&
+        e.scene.wavelength == L.wavelength && e.scene.pitch == L.pitch && e.scene.z == L.z) {
+      e.stamp = ++g_stamp;
+      return e.h;
+    }
+    wcgh_lut_destroy(e.h);
+    g_luts.erase(it);
+  }
+  if (g_luts.size() >= kMaxLuts) {
+    auto oldest = std::min_element(g_luts.begin(), g_luts.end(), [](const auto& a, const auto& b) {
+      return a.second.stamp < b.second.stamp;
+    });
+    wcgh_lut_destroy(oldest->second.h);
+    g_luts.erase(oldest);
+  }
+  LutEntry e;
+  e.count = sup.size();
+  e.scene = L;
+  e.block = lut.block_size();
+  e.hash = hash;
+  e.stamp = ++g_stamp;
+  check(wcgh_lut_create(gpu(), &L, lut.scene().plane_size(), lut.block_size(), sup.data(), WCGH_F64,
+                        &e.h));
+  g_luts[key] = e;
+  return e.h;
+}
+
+// One device plane per size for the calls on host ComplexFields: the stage's
+// contribution is formed on the device and added to the caller's plane.
+std::mutex g_plane_mu;
+wcgh_plane* scratch_plane(int n) {
+  static std::map<int, wcgh_plane*> planes;
+  auto it = planes.find(n);
+  if (it == planes.end()) {
+    wcgh_plane* p = nullptr;
+    check(wcgh_plane_create(gpu(), n, &p));
+    it = planes.emplace(n, p).first;
+  } else {
+    check(wcgh_plane_zero(it->second));
+  }
+  return it->second;
+}
+
+void add_plane_into(ComplexField& plane, wcgh_plane* dev) {
+  std::vector<std::complex<double>> c(plane.size());
+  check(wcgh_plane_download(dev, c.data(), WCGH_F64));
+  for (std::size_t i = 0; i < plane.size(); ++i) plane.data()[i] += c[i];
 }
 
 }  // namespace
@@ -219,22 +307,15 @@ void apply_block(ComplexField& plane, const FringeLut& lut, GridCell cell,
   if (cell.x < 0 || cell.y < 0 || cell.x >= cells || cell.y >= cells)
     throw ValidationError("apply_block: cell (" + std::to_string(cell.x) + "," +
                           std::to_string(cell.y) + ") out of range");
-  const wcgh_layer L = layer_of(lut.scene());
+  // the caller's samples (synthesis.cpp:18-42), complex weight as re + i im
+  wcgh_lut* dl = device_lut(lut);
   const uint32_t idx = uint32_t(cell.y) * uint32_t(cells) + uint32_t(cell.x);
-  for (int part = 0; part < 2; ++part) {  // real, then imaginary weight (i * S)
-    const float w = float(part == 0 ? weight.real() : weight.imag());
-    if (w == 0.0f) continue;
-    std::vector<float> c(2 * plane.size(), 0.0f);
-    uint64_t ops = 0;
-    check(wcgh_apply_blocks(gpu(), &L, n, b, &idx, &w, 1, c.data(), &ops));
-    if (part == 1)
-      for (std::size_t i = 0; i < plane.size(); ++i) {
-        const float re = c[2 * i], im = c[2 * i + 1];
-        c[2 * i] = -im;
-        c[2 * i + 1] = re;
-      }
-    add_into(plane, c);
-  }
+  const float wr = float(weight.real()), wi = float(weight.imag());
+  uint64_t ops = 0;
+  std::lock_guard<std::mutex> lk(g_plane_mu);
+  wcgh_plane* dev = scratch_plane(n);
+  check(wcgh_lut_apply_blocks(dl, &idx, &wr, wi != 0.0f ? &wi : nullptr, 1, dev, &ops));
+  add_plane_into(plane, dev);
   counter.add(level, 1);
 }
 
@@ -253,13 +334,15 @@ ComplexField synthesize_base(const HaarPyramid& pyramid, const SaliencyPyramid& 
     cells[i] = uint32_t(i);
     w[i] = float(pyramid.approx.data()[i]);
   }
-  std::vector<float> c(2 * std::size_t(n) * n, 0.0f);
+  wcgh_lut* dl = device_lut(lut);
   uint64_t ops = 0;
-  const wcgh_layer L = layer_of(lut.scene());
-  check(wcgh_apply_blocks(gpu(), &L, n, block, cells.data(), w.data(), int64_t(cells.size()),
-                          c.data(), &ops));
+  ComplexField out(n, n);
+  std::lock_guard<std::mutex> lk(g_plane_mu);
+  wcgh_plane* dev = scratch_plane(n);
+  check(wcgh_lut_apply_blocks(dl, cells.data(), w.data(), nullptr, int64_t(cells.size()), dev, &ops));
+  check(wcgh_plane_download(dev, out.data().data(), WCGH_F64));
   counter.add(OpLevel::kBaseLll, ops);
-  return widen(c, n);
+  return out;
 }
 
 void refine(ComplexField& plane, const RealImage& h, const RealImage& v, const RealImage& d,
@@ -275,13 +358,16 @@ void refine(ComplexField& plane, const RealImage& h, const RealImage& v, const R
     throw ValidationError("refine: saliency level does not match the residual resolution");
   if (2 * m * lut.block_size() != n)
     throw ValidationError("refine: LUT block size does not match the residual level");
-  std::vector<float> c(2 * plane.size(), 0.0f);
   std::vector<uint8_t> on(std::size_t(4) * m * m);
   uint64_t ops = 0;
-  const wcgh_layer L = layer_of(lut.scene());
-  check(wcgh_refine(gpu(), &L, n, h.data().data(), v.data().data(), d.data().data(), m,
-                    saliency_finer.data().data(), threshold, c.data(), on.data(), &ops));
-  add_into(plane, c);
+  wcgh_lut* dl = device_lut(lut);
+  {
+    std::lock_guard<std::mutex> lk(g_plane_mu);
+    wcgh_plane* dev = scratch_plane(n);
+    check(wcgh_lut_refine(dl, h.data().data(), v.data().data(), d.data().data(), m,
+                          saliency_finer.data().data(), threshold, dev, on.data(), &ops));
+    add_plane_into(plane, dev);
+  }
   counter.add(level, ops);
   if (mask) *mask = GateMask{2 * m, 2 * m, std::move(on)};
 }
@@ -302,7 +388,8 @@ int method_code(SynthesisMethod m) {
 ProgressiveResult run_progressive(const std::vector<const RealImage*>& objects,
                                   const std::vector<const RealImage*>& saliencies,
                                   const std::vector<SceneParams>& scenes, const RefinementPlan& plan,
-                                  int method, std::optional<std::uint64_t> seed = {}) {
+                                  int method, std::optional<std::uint64_t> seed = {},
+                                  const LutSet* luts = nullptr) {
   plan.validate();
   const int L = int(scenes.size());
   if (L < 1 || int(objects.size()) != L || int(saliencies.size()) != L)
@@ -347,7 +434,17 @@ ProgressiveResult run_progressive(const std::vector<const RealImage*>& objects,
   check(wcgh_job_create(gpu(), &d, &job));
   std::vector<float> stages(std::size_t(8) * n * n);
   wcgh_stats st{};
-  int rc = wcgh_job_upload(job, obj.data(), sal.data());
+  int rc = WCGH_OK;
+  if (luts) {  // the caller's LutSet (synthesize_progressive reads luts.of(B), synthesis.cpp:230-250)
+    try {
+      for (int b : kLutBlockSizes)
+        if (!rc) rc = wcgh_job_use_lut(job, 0, device_lut(luts->of(b)));
+    } catch (...) {
+      wcgh_job_destroy(job);
+      throw;
+    }
+  }
+  if (!rc) rc = wcgh_job_upload(job, obj.data(), sal.data());
   if (!rc) rc = wcgh_job_run(job);
   if (!rc) rc = wcgh_job_download_stages(job, stages.data());
   if (!rc) rc = wcgh_job_stats(job, &st);
@@ -397,7 +494,8 @@ ProgressiveResult synthesize_progressive(const RealImage& object, const RealImag
   if (!(luts.of(1).scene() == scene))
     throw ValidationError("synthesize_progressive: LUTs built for a different scene");
   // the reference's algorithm (its LutSet argument)
-  return run_progressive({&object}, {&saliency}, {scene}, plan, WCGH_METHOD_LUT, random_phase_seed);
+  return run_progressive({&object}, {&saliency}, {scene}, plan, WCGH_METHOD_LUT, random_phase_seed,
+                         &luts);
 }
 
 ProgressiveResult synthesize_progressive(const RealImage& object, const RealImage& saliency,
@@ -426,10 +524,10 @@ ComplexField synthesize_pointwise_oracle(const RealImage& object, const ScenePar
     throw ValidationError("pointwise oracle: object size does not match the scene");
   if (unit_lut.block_size() != 1) throw ValidationError("pointwise oracle: needs the 1x1 LUT");
   if (!(unit_lut.scene() == scene)) throw ValidationError("pointwise oracle: LUT built for a different scene");
-  // every object pixel through the 1x1 LUT = the B=1 superposition of all pixels
-  const wcgh_layer L = layer_of(scene);
+  // every object pixel through the caller's 1x1 LUT = the B=1 superposition
+  // of all pixels, complex weights as re + i im (synthesis.cpp:269-284)
   std::vector<uint32_t> cells(std::size_t(n) * n);
-  std::vector<float> w(cells.size());
+  std::vector<float> wr(cells.size()), wi;
   for (std::size_t i = 0; i < cells.size(); ++i) {
     cells[i] = uint32_t(i);
     if (!std::isfinite(object.data()[i])) throw ValidationError("object: non-finite sample");
@@ -437,20 +535,20 @@ ComplexField synthesize_pointwise_oracle(const RealImage& object, const ScenePar
   std::optional<ComplexField> rotated;
   if (random_phase_seed) rotated = random_phase_field(object, *random_phase_seed);
   for (std::size_t i = 0; i < cells.size(); ++i)
-    w[i] = float(rotated ? rotated->data()[i].real() : object.data()[i]);
-  std::vector<float> c(2 * cells.size(), 0.0f);
-  uint64_t ops = 0;
-  check(wcgh_apply_blocks(gpu(), &L, n, 1, cells.data(), w.data(), int64_t(cells.size()), c.data(), &ops));
-  counter.add(OpLevel::kPointwiseOracle, ops);
-  ComplexField out = widen(c, n);
-  if (rotated) {  // complex weights (synthesis.cpp:269-284): + i * the imaginary superposition
-    for (std::size_t i = 0; i < cells.size(); ++i) w[i] = float(rotated->data()[i].imag());
-    std::fill(c.begin(), c.end(), 0.0f);
-    uint64_t ops_im = 0;
-    check(wcgh_apply_blocks(gpu(), &L, n, 1, cells.data(), w.data(), int64_t(cells.size()), c.data(), &ops_im));
-    for (std::size_t i = 0; i < cells.size(); ++i)
-      out.data()[i] += std::complex<double>(-double(c[2 * i + 1]), double(c[2 * i]));
+    wr[i] = float(rotated ? rotated->data()[i].real() : object.data()[i]);
+  if (rotated) {
+    wi.resize(cells.size());
+    for (std::size_t i = 0; i < cells.size(); ++i) wi[i] = float(rotated->data()[i].imag());
   }
+  wcgh_lut* dl = device_lut(unit_lut);
+  uint64_t ops = 0;
+  ComplexField out(n, n);
+  std::lock_guard<std::mutex> lk(g_plane_mu);
+  wcgh_plane* dev = scratch_plane(n);
+  check(wcgh_lut_apply_blocks(dl, cells.data(), wr.data(), rotated ? wi.data() : nullptr,
+                              int64_t(cells.size()), dev, &ops));
+  check(wcgh_plane_download(dev, out.data().data(), WCGH_F64));
+  counter.add(OpLevel::kPointwiseOracle, ops);
   return out;
 }
 
