@@ -12,6 +12,10 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libwcgh.so"
+# WCGH_CHECKED=1 loads the checked build (same sources, -DWCGH_CHECKED: device
+# bounds checks + poisoned scratch; test use only, built by build(checked=True))
+if os.environ.get("WCGH_CHECKED") == "1":
+    LIB_PATH = LIB_PATH.with_name("libwcgh_checked.so")
 
 WCGH_OK, WCGH_EVALIDATION, WCGH_ERUNTIME = 0, 1, 2
 U8, F32, F64, C128 = 0, 1, 2, 3
@@ -142,7 +146,7 @@ def load() -> C.CDLL:
         return _lib
     if not LIB_PATH.exists():
         from . import build as _build
-        _build.build()
+        _build.build(checked=LIB_PATH.name == "libwcgh_checked.so")
     lib = C.CDLL(str(LIB_PATH))
     for name, res, args in _SIGS:
         fn = getattr(lib, name)

@@ -32,27 +32,42 @@ def _run(cmd: list[str], log: Path | None = None) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """libwcgh.so (the product), or with checked=True libwcgh_checked.so: the
+    same sources with -DWCGH_CHECKED (device bounds checks, poisoned scratch;
+    test use only, loaded when WCGH_CHECKED=1). Translation units compile in
+    parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    out_dir = BUILD.parent / ("wcgh_checked" if checked else "wcgh")
+    lib = PKG / ("libwcgh_checked.so" if checked else "libwcgh.so")
+    out_dir.mkdir(parents=True, exist_ok=True)
     deps = [CSRC / s for s in SOURCES] + [CSRC / "wcgh_internal.cuh", CSRC / "wcgh_state.cuh",
                                            ROOT / "include" / "wcgh.h"]
     newest = max(p.stat().st_mtime for p in deps)
-    if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
-        return LIB
-    objs = []
-    for src in SOURCES:
-        obj = BUILD / (Path(src).stem + ".o")
-        _run([NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)],
-             log=BUILD / (Path(src).stem + ".ptxas.log"))
-        objs.append(str(obj))
-        if verbose:
-            print((BUILD / (Path(src).stem + ".ptxas.log")).read_text())
-    tmp = LIB.with_suffix(".so.tmp")
+    if lib.exists() and lib.stat().st_mtime >= newest and not force:
+        return lib
+    extra = ["-DWCGH_CHECKED"] if checked else []
+
+    def one(src):
+        obj = out_dir / (Path(src).stem + ".o")
+        _run([NVCC, *ARCH, *FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)],
+             log=out_dir / (Path(src).stem + ".ptxas.log"))
+        return str(obj)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(one, SOURCES))
+    if verbose:
+        for src in SOURCES:
+            print((out_dir / (Path(src).stem + ".ptxas.log")).read_text())
+    tmp = lib.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lcufft", "-lrt", "-ldl",
           "-lpthread", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
-    tmp.replace(LIB)
-    return LIB
+    tmp.replace(lib)
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build(force="--force" in sys.argv, checked=True))

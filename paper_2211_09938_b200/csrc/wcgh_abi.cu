@@ -13,6 +13,33 @@ using namespace wcgh::abi;
 
 thread_local std::string wcgh::abi::t_last_error;
 
+#ifdef WCGH_CHECKED
+namespace wcgh {
+namespace chk {
+void collect_wcgh_analysis();
+void collect_wcgh_direct();
+void collect_wcgh_lut();
+void collect_wcgh_fft();
+void collect_wcgh_recon();
+void collect_wcgh_abi();
+void collect_wcgh_job();
+void collect_wcgh_io();
+void collect_wcgh_lutobj();
+void collect_all() {
+  collect_wcgh_analysis();
+  collect_wcgh_direct();
+  collect_wcgh_lut();
+  collect_wcgh_fft();
+  collect_wcgh_recon();
+  collect_wcgh_abi();
+  collect_wcgh_job();
+  collect_wcgh_io();
+  collect_wcgh_lutobj();
+}
+}  // namespace chk
+}  // namespace wcgh
+#endif
+
 extern "C" {
 
 int wcgh_abi_version(void) { return WCGH_ABI_VERSION; }
@@ -566,3 +593,5 @@ int wcgh_ssim(wcgh_ctx* ctx, const double* a, const double* b, int width, int he
 }
 
 }  // extern "C"
+
+WCGH_CHK_TU(wcgh_abi)

@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(256) k_compact_points(const float* __restrict_
     dst += __popc(b);
     if (dst_im) dst_im += __popc(b);
   }
+  // K1's per-segment count (scanned into offsets) must equal the nonzeros
+  // this warp found: records of neighbouring segments never overlap
+  WCGH_DCHECK(dst - (reinterpret_cast<int4*>(points) + offsets[gw]) == offsets[gw + 1] - offsets[gw]);
 }
 
 // Stage contribution images for the snapshots of the direct and FFT
@@ -982,3 +985,5 @@ int launch_seg_counts_f32(const float* img, int n, int n_layers, int* counts, cu
 }
 
 }  // namespace wcgh
+
+WCGH_CHK_TU(wcgh_analysis)

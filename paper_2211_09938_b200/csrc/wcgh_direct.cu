@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
-      for (int i = threadIdx.x; i < nb; i += kThreads) sp[i] = pts[b + i];
+      for (int i = threadIdx.x; i < nb; i += kThreads) {
+        WCGH_DCHECK(b + i < n_points && b + i >= 0);
+        sp[i] = pts[b + i];
+      }
       __syncthreads();
 
 #pragma unroll 2
@@ -193,6 +196,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int x = xb + 32 * i;
       const float2 r = i & 1 ? make_float2(re2[i / 2].y, im2[i / 2].y)
                              : make_float2(re2[i / 2].x, im2[i / 2].x);
+      WCGH_DCHECK(x >= nh || size_t(blockIdx.y) * out_chunk_stride + size_t(row) * nh + x <
+                                 size_t(gridDim.y) * out_chunk_stride);
       if (x < nh) dst[x] = r;
     }
   }
@@ -543,3 +548,5 @@ int launch_band_to_peers(const float2* band_dev, size_t count, const PeerPlanes&
 }
 
 }  // namespace wcgh
+
+WCGH_CHK_TU(wcgh_direct)

@@ -176,3 +176,5 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
 }
 
 }  // namespace wcgh
+
+WCGH_CHK_TU(wcgh_fft)

@@ -35,6 +35,50 @@ inline void require(bool ok, const std::string& what) {
   if (!ok) throw ValidationError(what);
 }
 
+// ---- checked build (-DWCGH_CHECKED, libwcgh_checked.so; test use only) -------
+// compute-sanitizer is not available on the GPU pool, so a separate build of
+// the same sources carries its own checks: WCGH_DCHECK(cond) in the kernels
+// records the first failing source line in a per-translation-unit device
+// flag (the kernel continues; the offending access is still performed only
+// where it is provably inside an allocation); every C-ABI call collects the
+// flags after its work (abi::guard) and turns a hit into WCGH_ERUNTIME
+// "checked build: ...". Scratch allocations are poisoned with 0xFF bytes
+// (NaN floats, -1 ints), so a read of memory no kernel wrote shows up in
+// the results. The product library (libwcgh.so) compiles none of this.
+#ifdef WCGH_CHECKED
+namespace chk {
+static __device__ unsigned int d_fail;
+static __device__ unsigned int d_line;
+__device__ __forceinline__ void fail(unsigned line) {
+  if (atomicCAS(&d_fail, 0u, 1u) == 0u) d_line = line;
+}
+// reads and clears this translation unit's flag; throws on a hit
+inline void collect_tu(const char* tu) {
+  cudaDeviceSynchronize();  // the ABI's streams are non-blocking; the flag is read on the legacy stream
+  unsigned f = 0, l = 0;
+  if (cudaMemcpyFromSymbol(&f, d_fail, sizeof(f)) != cudaSuccess) return;
+  if (!f) return;
+  cudaMemcpyFromSymbol(&l, d_line, sizeof(l));
+  const unsigned zero = 0;
+  cudaMemcpyToSymbol(d_fail, &zero, sizeof(zero));
+  throw RuntimeError(std::string("checked build: device bounds check failed at ") + tu + ":" +
+                     std::to_string(l));
+}
+void collect_all();  // every translation unit (wcgh_abi.cu)
+}  // namespace chk
+#define WCGH_DCHECK(cond)                                   \
+  do {                                                      \
+    if (!(cond)) ::wcgh::chk::fail(unsigned(__LINE__));     \
+  } while (0)
+#define WCGH_CHK_TU(NAME) \
+  namespace wcgh { namespace chk { void collect_##NAME() { collect_tu(#NAME ".cu"); } } }
+#else
+#define WCGH_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#define WCGH_CHK_TU(NAME)
+#endif
+
 // RAII device buffer.
 struct DevBuf {
   void* p = nullptr;
@@ -55,6 +99,9 @@ struct DevBuf {
     if (n == 0) n = 16;
     WCGH_CUDA(cudaMalloc(&p, n));
     bytes = n;
+#ifdef WCGH_CHECKED
+    WCGH_CUDA(cudaMemset(p, 0xFF, n));  // poison: reads of unwritten scratch show up as NaN / -1
+#endif
     return p;
   }
   template <typename T>
@@ -74,12 +121,15 @@ struct PeerPlanes {
   float2* p[kMaxPeers];
   int n = 0;
   size_t offset = 0;
+  size_t limit = 0;  // elements in each full plane (plane_size^2)
 };
 __device__ __forceinline__ void store_peers(const PeerPlanes& pp, size_t i, float2 v) {
+  if (pp.n) WCGH_DCHECK(pp.offset + i < pp.limit);
   for (int k = 0; k < pp.n; ++k) pp.p[k][pp.offset + i] = v;
 }
 // two adjacent pixels (i even, offset even, peer planes 16-byte aligned) as one float4
 __device__ __forceinline__ void store_peers2(const PeerPlanes& pp, size_t i, float4 v) {
+  if (pp.n) WCGH_DCHECK(pp.offset + i + 1 < pp.limit);
   for (int k = 0; k < pp.n; ++k) *reinterpret_cast<float4*>(pp.p[k] + pp.offset + i) = v;
 }
 inline bool peers_aligned16(const PeerPlanes& pp) {

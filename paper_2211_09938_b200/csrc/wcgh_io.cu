@@ -133,3 +133,5 @@ int wcgh_read_cghl(const char* path, float* lut, int64_t capacity, int* n_out, i
 }
 
 }  // extern "C"
+
+WCGH_CHK_TU(wcgh_io)

@@ -2,10 +2,16 @@
 // / fused multi-GPU gather) and the one-shot entry points.
 #include <thread>
 
+#include <cstdlib>
+
 #include "wcgh_state.cuh"
 
 using namespace wcgh;
 using namespace wcgh::abi;
+
+#ifdef WCGH_CHECKED
+__global__ void k_inject_one(int* c) { *c += 1; }  // checked-build negative control
+#endif
 
 void wcgh::abi::job_validate(const wcgh_desc& d) {
   require(d.n_layers >= 1 && d.n_layers <= kMaxLayers, "job: n_layers must be 1..16");
@@ -198,6 +204,15 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
   const size_t per_layer = size_t(No) * seg_per_row(No);
   const size_t nseg = per_layer * L;
   const bool fft = d.method == WCGH_METHOD_FFT;
+#ifdef WCGH_CHECKED
+  // negative control of the checked build: one extra count in the last
+  // segment makes K2's record count disagree with K1's (caught by the
+  // compaction check; all writes stay inside the point buffer)
+  if (const char* e = std::getenv("WCGH_CHK_INJECT"); e && std::string(e) == "segcount") {
+    k_inject_one<<<1, 1, 0, s>>>(j->seg_counts.as<int>() + nseg - 1);
+    WCGH_CHECK_LAUNCH();
+  }
+#endif
   const int scan_launches = launch_scan(j->seg_counts.as<int>(), j->seg_offsets.as<int>(), int(nseg), s,
                                         &j->scan_scratch);
   const bool cplx = j->complex_obj();
@@ -493,6 +508,7 @@ int wcgh_job_set_peer_planes(wcgh_job* job, void* const* planes_dev, int n_plane
     }
     pp.n = n_planes;
     pp.offset = size_t(job->desc.row0) * size_t(job->desc.plane_size);
+    pp.limit = size_t(job->desc.plane_size) * size_t(job->desc.plane_size);
     job->peers = pp;
   });
 }
@@ -747,3 +763,4 @@ int wcgh_synthesize_multi(int n_devices, const int* devices, const wcgh_desc* de
 
 }  // extern "C"
 
+WCGH_CHK_TU(wcgh_job)

@@ -196,10 +196,22 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
   };
   const int r_lo = lower_bound(d_lo), r_hi = lower_bound(d_hi);
   int w_lo = 0;
+#ifdef WCGH_CHECKED
+  unsigned smem_floats;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(smem_floats));
+  smem_floats /= 4;
+  // the guarded LUT allocation (lut_alloc_bytes): every window / prefetch read
+  const float2* lut_lo = lut - size_t(kLutGuardBefore) * span;
+  const float2* lut_hi = lut + size_t(span + kLutGuardAfter) * span + kLutPadCols;
+#define WCGH_LUT_IN(ptr) WCGH_DCHECK((ptr) >= lut_lo && (ptr) + 32 * (PX - 1) < lut_hi)
+#else
+#define WCGH_LUT_IN(ptr)
+#endif
   if (r_lo < r_hi) {
     w_lo = __ldg(&runs[r_lo].w);
     const int4 lr = __ldg(runs + r_hi - 1);
     const int w_n = lr.w + lr.z - w_lo;
+    WCGH_DCHECK(w_n + S - 1 <= int(smem_floats));  // incl. the remainder's up-front reads
     for (int i = threadIdx.x; i < w_n; i += W * 32) s_w[i] = __ldg(dense + w_lo + i);
   }
   __syncthreads();
@@ -230,6 +242,7 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
       const float2* rt = rp - D * row_step;
 #pragma unroll
       for (int t = -D; t < R; ++t) {
+        WCGH_LUT_IN(rt);
 #pragma unroll
         for (int i = 0; i < PX; ++i) ring[(t + S) % S][i] = __ldg(rt + 32 * i);
         rt += row_step;
@@ -248,6 +261,7 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
         acc[j][i] = ffma2(wv, ring[(j - (uu) + 2 * S) % S][i], acc[j][i]);      \
       }                                                                         \
     }                                                                           \
+    WCGH_LUT_IN(pf);                                                            \
     _Pragma("unroll") for (int i = 0; i < PX; ++i)                              \
       ring[(R - 1 - (uu) + S) % S][i] = __ldg(pf + 32 * i);                     \
     pf -= row_step;                                                             \
@@ -273,6 +287,7 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
 #undef WCGH_LUT_STEP
   }
 
+#undef WCGH_LUT_IN
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int row = yb + j * B;
@@ -281,6 +296,8 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
 #pragma unroll
       for (int i = 0; i < PX; ++i) {
         const int x = x0 + 32 * i;
+        WCGH_DCHECK(size_t(blockIdx.y) * out_stride + size_t(row) * nh + x < size_t(gridDim.y) * out_stride ||
+                    x >= nh);
         if (x < nh) dst[x] = acc[j][i];
       }
     }
@@ -490,3 +507,5 @@ int launch_lut_dense(const float2* lut, int nh, int block, const float* w, int m
 }
 
 }  // namespace wcgh
+
+WCGH_CHK_TU(wcgh_lut)

@@ -294,3 +294,5 @@ int wcgh_job_use_lut(wcgh_job* job, int layer, const wcgh_lut* lut) {
 }
 
 }  // extern "C"
+
+WCGH_CHK_TU(wcgh_lutobj)

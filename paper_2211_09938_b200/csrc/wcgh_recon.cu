@@ -274,3 +274,5 @@ int launch_ssim(const double* a, const double* b, int w, int h, int window, doub
 }
 
 }  // namespace wcgh
+
+WCGH_CHK_TU(wcgh_recon)

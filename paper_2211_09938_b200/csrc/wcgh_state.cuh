@@ -109,6 +109,9 @@ int guard(const wcgh_ctx* ctx, F&& f) {
   (void)ctx;
   try {
     f();
+#ifdef WCGH_CHECKED
+    chk::collect_all();
+#endif
     return WCGH_OK;
   } catch (const ValidationError& e) {
     t_last_error = e.what();
