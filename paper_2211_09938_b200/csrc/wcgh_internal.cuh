@@ -56,7 +56,10 @@ __device__ __forceinline__ void fail(unsigned line) {
 inline void collect_tu(const char* tu) {
   cudaDeviceSynchronize();  // the ABI's streams are non-blocking; the flag is read on the legacy stream
   unsigned f = 0, l = 0;
-  if (cudaMemcpyFromSymbol(&f, d_fail, sizeof(f)) != cudaSuccess) return;
+  const cudaError_t e = cudaMemcpyFromSymbol(&f, d_fail, sizeof(f));
+  if (e != cudaSuccess)
+    throw RuntimeError(std::string("checked build: cannot read the check flag of ") + tu + ": " +
+                       cudaGetErrorString(e));
   if (!f) return;
   cudaMemcpyFromSymbol(&l, d_line, sizeof(l));
   const unsigned zero = 0;
@@ -100,7 +103,11 @@ struct DevBuf {
     WCGH_CUDA(cudaMalloc(&p, n));
     bytes = n;
 #ifdef WCGH_CHECKED
-    WCGH_CUDA(cudaMemset(p, 0xFF, n));  // poison: reads of unwritten scratch show up as NaN / -1
+    // poison: reads of unwritten scratch show up as NaN / -1. The legacy
+    // stream does not order against the ABI's non-blocking streams: finish
+    // the fill before any stream work can touch the buffer.
+    WCGH_CUDA(cudaMemset(p, 0xFF, n));
+    WCGH_CUDA(cudaDeviceSynchronize());
 #endif
     return p;
   }
