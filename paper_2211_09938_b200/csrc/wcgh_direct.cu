@@ -371,7 +371,15 @@ void launch_fixed_nc(const DirectPlan& plan, const LaunchArgs& a) {
     launch_fixed_amp<P, 8>(plan, a);
 }
 
-int pixels_per_thread(int nh) { return nh >= 1024 ? 32 : (nh >= 512 ? 16 : 4); }
+int pixels_per_thread(int nh) {
+  // WCGH_DIRECT_P (16 or 32, nh >= 1024 only) overrides: tuning experiments
+  static const int forced = [] {
+    const char* e = std::getenv("WCGH_DIRECT_P");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (nh >= 1024 && (forced == 16 || forced == 32)) return forced;
+  return nh >= 1024 ? 32 : (nh >= 512 ? 16 : 4);
+}
 
 }  // namespace
 
@@ -442,6 +450,9 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
   }
   plan.n_corr = need <= 2 ? 2 : (need <= 3 ? 3 : (need <= 5 ? 5 : 8));
   plan.amp_degree = amp_rsqrt ? 0 : (amp3 ? 3 : (amp2 ? 2 : 1));
+  // WCGH_DIRECT_AMP (0..3) forces the amplitude series degree: tuning
+  // experiments only (it can exceed the 2e-6 truncation budget)
+  if (const char* e = std::getenv("WCGH_DIRECT_AMP")) plan.amp_degree = std::max(0, std::min(3, std::atoi(e)));
   return plan;
 }
 
