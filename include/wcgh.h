@@ -204,6 +204,17 @@ int wcgh_refine(wcgh_ctx* ctx, const wcgh_layer* scene, int n, const double* h, 
                 const double* d, int m, const double* saliency_finer, double threshold,
                 float* plane, uint8_t* mask_out, uint64_t* ops_out);
 
+/* The reference's small helpers, on the device (no host arithmetic in the
+ * drop-in): haar_synthesize (haar.hpp:43, haar.cpp:76-86; the pyramid in
+ * wcgh_haar_analyze's flat layout, out n x n, bit-identical),
+ * upsample_replicate (haar.hpp:51, haar.cpp:98-109; out (w*f) x (h*f),
+ * bit-identical) and point_fringe (fringe_lut.hpp:15, fringe_lut.cpp:27-32;
+ * out2 = (re, im) in fp64, the device sin/cos within 2 ulp of the host's). */
+int wcgh_haar_synthesize(wcgh_ctx* ctx, const double* pyramid, int n, int levels, double* out);
+int wcgh_upsample_replicate(wcgh_ctx* ctx, const double* coarse, int width, int height, int factor,
+                            double* out);
+int wcgh_point_fringe(wcgh_ctx* ctx, const wcgh_layer* scene, int dx, int dy, double* out2);
+
 /* ---- device-resident LUTs and planes (the caller's FringeLut / ComplexField)
  * The reference's apply_block / synthesize_base / refine read the CALLER's
  * FringeLut samples (lut.support(), synthesis.cpp:18-42,149-178), which may

@@ -204,24 +204,23 @@ HaarPyramid haar_analyze(const RealImage& image, int levels) {
 }
 
 RealImage haar_synthesize(const HaarPyramid& pyramid) {
-  // exact inverse (validation helper, not on the synthesis path)
+  // the exact inverse (validation helper), on the device in the reference's order
   if (pyramid.details.empty()) throw ValidationError("haar_synthesize: empty pyramid");
-  RealImage cur = pyramid.approx;
+  if (pyramid.approx.width() != pyramid.approx.height())
+    throw ValidationError("haar_synthesize: pyramid must be square (haar_analyze's)");
+  RealImage cur_check = pyramid.approx;
   for (auto it = pyramid.details.rbegin(); it != pyramid.details.rend(); ++it) {
-    if (!cur.same_size(it->h)) throw ValidationError("haar_synthesize: subband sizes inconsistent");
-    const int m = cur.width();
-    RealImage out(2 * m, 2 * m);
-    for (int y = 0; y < m; ++y)
-      for (int x = 0; x < m; ++x) {
-        const double a = cur.at(x, y), h = it->h.at(x, y), v = it->v.at(x, y), d = it->d.at(x, y);
-        out.at(2 * x, 2 * y) = a + h + v + d;
-        out.at(2 * x + 1, 2 * y) = a - h + v - d;
-        out.at(2 * x, 2 * y + 1) = a + h - v - d;
-        out.at(2 * x + 1, 2 * y + 1) = a - h - v + d;
-      }
-    cur = std::move(out);
+    if (!cur_check.same_size(it->h) || !it->h.same_size(it->v) || !it->h.same_size(it->d))
+      throw ValidationError("haar_synthesize: subband sizes inconsistent");
+    cur_check = RealImage(2 * cur_check.width(), 2 * cur_check.height());
   }
-  return cur;
+  const int n = cur_check.width(), levels = int(pyramid.details.size());
+  std::vector<double> flat(pyramid.approx.data().begin(), pyramid.approx.data().end());
+  for (const auto& b : pyramid.details)
+    for (const RealImage* im : {&b.h, &b.v, &b.d}) flat.insert(flat.end(), im->data().begin(), im->data().end());
+  std::vector<double> out(std::size_t(n) * n);
+  check(wcgh_haar_synthesize(gpu(), flat.data(), n, levels, out.data()));
+  return RealImage(n, n, std::move(out));
 }
 
 RealImage expand_residual(const RealImage& h, const RealImage& v, const RealImage& d) {
@@ -236,10 +235,10 @@ RealImage expand_residual(const RealImage& h, const RealImage& v, const RealImag
 RealImage upsample_replicate(const RealImage& coarse, int factor) {
   if (factor < 2 || (factor & (factor - 1)) != 0)
     throw ValidationError("upsample_replicate: factor must be a power of two >= 2");
-  RealImage out(coarse.width() * factor, coarse.height() * factor);
-  for (int y = 0; y < out.height(); ++y)
-    for (int x = 0; x < out.width(); ++x) out.at(x, y) = coarse.at(x / factor, y / factor);
-  return out;
+  std::vector<double> out(std::size_t(coarse.width()) * factor * std::size_t(coarse.height()) * factor);
+  check(wcgh_upsample_replicate(gpu(), coarse.data().data(), coarse.width(), coarse.height(), factor,
+                                out.data()));
+  return RealImage(coarse.width() * factor, coarse.height() * factor, std::move(out));
 }
 
 // ---- saliency.hpp --------------------------------------------------------------
@@ -605,10 +604,11 @@ bool supported_block(int b) {
 }  // namespace
 
 std::complex<double> point_fringe(const SceneParams& scene, int dx, int dy) {
-  const double px = dx * scene.pitch();
-  const double py = dy * scene.pitch();
-  const double r = std::sqrt(px * px + py * py + scene.z() * scene.z());
-  return std::polar(1.0 / r, scene.wave_number() * r);
+  // fp64 on the device (fringe_lut.cpp:27-32; sin/cos within 2 ulp of the host's)
+  const wcgh_layer L = layer_of(scene);
+  double v[2];
+  check(wcgh_point_fringe(gpu(), &L, dx, dy, v));
+  return {v[0], v[1]};
 }
 
 FringeLut::FringeLut(SceneParams scene, int block_size, ComplexField support)

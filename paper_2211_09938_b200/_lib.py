@@ -117,6 +117,9 @@ _SIGS = [
                                  C.POINTER(Layer)]),
     ("wcgh_job_load_lut", C.c_int, [_VP, C.c_int, C.c_int, _VP]),
     ("wcgh_job_use_lut", C.c_int, [_VP, C.c_int, _VP]),
+    ("wcgh_haar_synthesize", C.c_int, [_VP, _VP, C.c_int, C.c_int, _VP]),
+    ("wcgh_upsample_replicate", C.c_int, [_VP, _VP, C.c_int, C.c_int, C.c_int, _VP]),
+    ("wcgh_point_fringe", C.c_int, [_VP, C.POINTER(Layer), C.c_int, C.c_int, _VP]),
     ("wcgh_lut_create", C.c_int, [_VP, C.POINTER(Layer), C.c_int, C.c_int, _VP, C.c_int,
                                   C.POINTER(_VP)]),
     ("wcgh_lut_destroy", None, [_VP]),

@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "wcgh"
 LIB = PKG / "libwcgh.so"
 SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_fft.cu", "wcgh_recon.cu",
-           "wcgh_abi.cu", "wcgh_job.cu", "wcgh_io.cu", "wcgh_lutobj.cu"]
+           "wcgh_abi.cu", "wcgh_job.cu", "wcgh_io.cu", "wcgh_lutobj.cu", "wcgh_helpers.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -25,6 +25,7 @@ void collect_wcgh_abi();
 void collect_wcgh_job();
 void collect_wcgh_io();
 void collect_wcgh_lutobj();
+void collect_wcgh_helpers();
 void collect_all() {
   collect_wcgh_analysis();
   collect_wcgh_direct();
@@ -35,6 +36,7 @@ void collect_all() {
   collect_wcgh_job();
   collect_wcgh_io();
   collect_wcgh_lutobj();
+  collect_wcgh_helpers();
 }
 }  // namespace chk
 }  // namespace wcgh

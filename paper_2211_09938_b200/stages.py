@@ -154,6 +154,35 @@ def refine(plane: np.ndarray, layer, h, v, d, saliency_finer, threshold: float, 
     return mask, int(ops.value)
 
 
+def haar_synthesize(pyramid_flat: np.ndarray, n: int, levels: int = 3, ctx=None) -> np.ndarray:
+    """haar_synthesize (haar.cpp:76-86) on the device from the flat pyramid of
+    haar_analyze: n x n doubles, bit-identical to the reference."""
+    flat = np.ascontiguousarray(pyramid_flat, np.float64)
+    out = np.empty((n, n))
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_haar_synthesize(c.h, L.ptr(flat), int(n), int(levels), L.ptr(out)))
+    return out
+
+
+def upsample_replicate(coarse: np.ndarray, factor: int, ctx=None) -> np.ndarray:
+    """upsample_replicate (haar.cpp:98-109) on the device."""
+    c_in = np.ascontiguousarray(coarse, np.float64)
+    h, w = c_in.shape
+    out = np.empty((h * factor, w * factor))
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_upsample_replicate(c.h, L.ptr(c_in), w, h, int(factor), L.ptr(out)))
+    return out
+
+
+def point_fringe(layer, dx: int, dy: int, ctx=None) -> complex:
+    """point_fringe (fringe_lut.cpp:27-32) in fp64 on the device."""
+    out = np.empty(2)
+    lay = L.Layer(*layer)
+    c = _ctx(ctx)
+    L.check(c.lib.wcgh_point_fringe(c.h, C.byref(lay), int(dx), int(dy), L.ptr(out)))
+    return complex(out[0], out[1])
+
+
 _CPLX = {np.dtype(np.complex64): L.F32, np.dtype(np.complex128): L.F64}
 
 

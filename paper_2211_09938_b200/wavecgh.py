@@ -179,21 +179,20 @@ def haar_analyze(image: np.ndarray, levels: int) -> HaarPyramid:
 
 
 def haar_synthesize(pyramid: HaarPyramid) -> np.ndarray:
-    """haar.cpp:76-86 (host validation helper)."""
+    """haar.cpp:76-86 (validation helper), on the device (bit-identical)."""
     if not pyramid.details:
         raise ValidationError("haar_synthesize: empty pyramid")
     cur = np.asarray(pyramid.approx, np.float64)
+    if cur.shape[0] != cur.shape[1]:
+        raise ValidationError("haar_synthesize: pyramid must be square (haar_analyze's)")
+    side = cur.shape[0]
     for b in reversed(pyramid.details):
-        if cur.shape != b.h.shape:
+        if (side, side) != b.h.shape or b.v.shape != b.h.shape or b.d.shape != b.h.shape:
             raise ValidationError("haar_synthesize: subband sizes inconsistent")
-        m = cur.shape[0]
-        out = np.empty((2 * m, 2 * m))
-        out[0::2, 0::2] = cur + b.h + b.v + b.d
-        out[0::2, 1::2] = cur - b.h + b.v - b.d
-        out[1::2, 0::2] = cur + b.h - b.v - b.d
-        out[1::2, 1::2] = cur - b.h - b.v + b.d
-        cur = out
-    return cur
+        side *= 2
+    flat = np.concatenate([cur.ravel()] + [np.concatenate([np.ravel(b.h), np.ravel(b.v), np.ravel(b.d)])
+                                           for b in pyramid.details])
+    return stages.haar_synthesize(flat, side, len(pyramid.details))
 
 
 def expand_residual(h: np.ndarray, v: np.ndarray, d: np.ndarray) -> np.ndarray:
@@ -205,10 +204,10 @@ def expand_residual(h: np.ndarray, v: np.ndarray, d: np.ndarray) -> np.ndarray:
 
 
 def upsample_replicate(coarse: np.ndarray, factor: int) -> np.ndarray:
-    """haar.cpp:98-109 (host helper)."""
+    """haar.cpp:98-109, on the device."""
     if factor < 2 or not is_power_of_two(factor):
         raise ValidationError("upsample_replicate: factor must be a power of two >= 2")
-    return np.kron(np.asarray(coarse, np.float64), np.ones((factor, factor)))
+    return stages.upsample_replicate(coarse, factor)
 
 
 # ---- saliency.hpp ---------------------------------------------------------------
@@ -253,14 +252,8 @@ LUT_BLOCK_SIZES = (1, 2, 4, 8)
 
 
 def point_fringe(scene: SceneParams, dx: int, dy: int) -> complex:
-    """fringe_lut.cpp:27-32: one unit point through the GPU accumulation
-    (fp64 phase mode), evaluated at one pixel."""
-    n = max(64, 1 << int(math.ceil(math.log2(2 * max(abs(dx), abs(dy)) + 2))))
-    c = n // 2
-    pts = np.zeros(1, L.POINT_DTYPE)
-    pts["x"], pts["y"], pts["a"] = c, c, 1.0
-    row = stages.synth_points(pts, [scene.layer()], n, row0=c + dy, rows=1, phase="fp64")
-    return complex(row[0, c + dx])
+    """fringe_lut.cpp:27-32 in fp64 on the device (sin/cos within 2 ulp)."""
+    return stages.point_fringe(scene.layer(), dx, dy)
 
 
 class FringeLut:
