@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "wcgh"
 LIB = PKG / "libwcgh.so"
 SOURCES = ["wcgh_analysis.cu", "wcgh_direct.cu", "wcgh_lut.cu", "wcgh_fft.cu", "wcgh_recon.cu",
-           "wcgh_abi.cu", "wcgh_job.cu", "wcgh_io.cu", "wcgh_lutobj.cu", "wcgh_helpers.cu"]
+           "wcgh_abi.cu", "wcgh_job.cu", "wcgh_io.cu", "wcgh_lutobj.cu", "wcgh_helpers.cu", "wcgh_fftk.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
         for src in SOURCES:
             print((out_dir / (Path(src).stem + ".ptxas.log")).read_text())
     tmp = lib.with_suffix(".so.tmp")
-    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lcufft", "-lrt", "-ldl",
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-ldl",
           "-lpthread", "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     tmp.replace(lib)
     return lib

@@ -26,6 +26,7 @@ void collect_wcgh_job();
 void collect_wcgh_io();
 void collect_wcgh_lutobj();
 void collect_wcgh_helpers();
+void collect_wcgh_fftk();
 void collect_all() {
   collect_wcgh_analysis();
   collect_wcgh_direct();
@@ -37,6 +38,7 @@ void collect_all() {
   collect_wcgh_io();
   collect_wcgh_lutobj();
   collect_wcgh_helpers();
+  collect_wcgh_fftk();
 }
 }  // namespace chk
 }  // namespace wcgh

@@ -3,12 +3,13 @@
 // (fringe_lut.cpp:27-32), evaluated as a circular correlation on an
 // L x L = 2Nh x 2Nh grid (L >= Nh + No - 1, so no wrap-around reaches the
 // output window). O(L^2 log L) instead of O(P Nh^2): an algorithm-class
-// alternative for dense objects, with cuFFT doing the transforms (library
-// code, like cuBLAS) and hand-written kernels for the fp64 fringe grid, the
-// scatter, the spectral product and the band extraction. Per-layer fringe
-// spectra are computed once per job (precompute, like the LUTs).
+// alternative for dense objects. Every kernel is hand-written: the fp64
+// fringe grid here, the transforms in wcgh_fftk.cu (shared-memory Stockham
+// row FFTs + tiled transposes, spectra kept in the transposed layout, the
+// object's zero padding, the spectral product and the band extraction fused
+// into the row passes). Per-layer fringe spectra are computed once per job
+// (precompute, like the LUTs).
 #include <cuda_runtime.h>
-#include <cufft.h>
 
 #include <cstdlib>
 #include <string>
@@ -17,14 +18,6 @@
 
 namespace wcgh {
 namespace {
-
-#define WCGH_CUFFT(call)                                                                       \
-  do {                                                                                         \
-    cufftResult r_ = (call);                                                                   \
-    if (r_ != CUFFT_SUCCESS)                                                                   \
-      throw RuntimeError(std::string("cuFFT error ") + std::to_string(int(r_)) + " at " +     \
-                         __FILE__ + ":" + std::to_string(__LINE__));                           \
-  } while (0)
 
 // F at every residue of the L x L grid: offsets d in [-(Nh-1), Nh-1] per axis
 // (the residue L/2 = Nh is never reached and stays zero). fp64 evaluation,
@@ -48,16 +41,6 @@ __global__ void k_fringe_grid(double wavelength, double pitch, double z, int nh,
   g[i] = make_float2(float(c / r), float(s / r));
 }
 
-// A_eff (No x No fp32, one layer; a_im: imaginary part or NULL) -> the L x L
-// grid at (off+y, off+x).
-__global__ void k_scatter(const float* __restrict__ a, const float* __restrict__ a_im, int no,
-                          int off, int L, float2* __restrict__ grid) {
-  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= size_t(no) * no) return;
-  const int x = int(i % no), y = int(i / no);
-  grid[size_t(off + y) * L + off + x] = make_float2(a[i], a_im ? a_im[i] : 0.f);
-}
-
 // acc (+)= fa * ff (complex), elementwise.
 __global__ void k_spec_mul(const float2* __restrict__ fa, const float2* __restrict__ ff, size_t n,
                            int accumulate, float2* __restrict__ acc) {
@@ -72,30 +55,6 @@ __global__ void k_spec_mul(const float2* __restrict__ fa, const float2* __restri
   acc[i] = r;
 }
 
-// out (rows x nh) = grid[row0 + y][x] / L^2.
-__global__ void k_extract(const float2* __restrict__ grid, int L, int nh, int row0, int rows,
-                          float scale, float2* __restrict__ out, PeerPlanes peers) {
-  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= size_t(rows) * nh) return;
-  const int x = int(i % nh), y = int(i / nh);
-  const float2 v = grid[size_t(row0 + y) * L + x];
-  const float2 r = make_float2(v.x * scale, v.y * scale);
-  out[i] = r;
-  store_peers(peers, i, r);  // fused row-tile gather
-}
-
-// Two pixels per thread (nh and L even): float4 grid loads, float4 complex64 stores.
-__global__ void k_extract2(const float4* __restrict__ grid, int L2h, int nh2, int row0, int rows,
-                           float scale, float4* __restrict__ out, PeerPlanes peers) {
-  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= size_t(rows) * nh2) return;
-  const int x = int(i % nh2), y = int(i / nh2);
-  const float4 v = grid[size_t(row0 + y) * L2h + x];
-  const float4 r = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
-  out[i] = r;
-  store_peers2(peers, 2 * i, r);  // fused row-tile gather
-}
-
 inline unsigned blocks_for(size_t n) { return unsigned((n + 255) / 256); }
 
 // WCGH_SYNC_DEBUG=1: synchronize after every step and name the failing one.
@@ -108,28 +67,21 @@ void dbg(cudaStream_t s, const char* tag) {
 
 }  // namespace
 
-FftPlan::~FftPlan() {
-  if (plan) cufftDestroy(plan);
-}
-
 void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cudaStream_t s) {
   const int L = 2 * nh;
   const size_t L2 = size_t(L) * L;
   fp.L = L;
   fp.n_layers = n_layers;
-  if (!fp.plan) WCGH_CUFFT(cufftPlan2d(&fp.plan, L, L, CUFFT_C2C));
-  WCGH_CUFFT(cufftSetStream(fp.plan, s));
+  fp.tw.ensure(L, s);
   float2* spec = static_cast<float2*>(fp.fringe_spec.reserve(sizeof(float2) * L2 * n_layers));
-  fp.grid.reserve(sizeof(float2) * L2);
-  fp.acc.reserve(sizeof(float2) * L2);
+  float2* g = static_cast<float2*>(fp.grid.reserve(sizeof(float2) * L2));
+  if (n_layers > 1) fp.acc.reserve(sizeof(float2) * L2);
   for (int l = 0; l < n_layers; ++l) {
-    float2* g = spec + L2 * l;
     k_fringe_grid<<<blocks_for(L2), 256, 0, s>>>(layers[l].wavelength, layers[l].pitch, layers[l].z,
                                                   nh, L, g);
     WCGH_CHECK_LAUNCH();
     dbg(s, "fringe_grid");
-    WCGH_CUFFT(cufftExecC2C(fp.plan, reinterpret_cast<cufftComplex*>(g),
-                            reinterpret_cast<cufftComplex*>(g), CUFFT_FORWARD));
+    fftk::forward_full(g, L, fp.tw, spec + L2 * l, fp.s1, fp.split, s);
     dbg(s, "fringe_fft");
   }
 }
@@ -139,40 +91,30 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
                          const PeerPlanes* peers, const float* a_im) {
   const int L = fp.L;
   const size_t L2 = size_t(L) * L;
-  WCGH_CUFFT(cufftSetStream(fp.plan, s));
   float2* grid = fp.grid.as<float2>();
-  float2* acc = fp.acc.as<float2>();
   int launches = 0;
   if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), s));
+  const size_t nn = size_t(no) * no;
   for (int l = 0; l < fp.n_layers; ++l) {
-    WCGH_CUDA(cudaMemsetAsync(grid, 0, sizeof(float2) * L2, s));
-    k_scatter<<<blocks_for(size_t(no) * no), 256, 0, s>>>(
-        a_eff + size_t(no) * no * l, a_im ? a_im + size_t(no) * no * l : nullptr, no, off, L, grid);
-    WCGH_CHECK_LAUNCH();
-    dbg(s, "scatter");
-    WCGH_CUFFT(cufftExecC2C(fp.plan, reinterpret_cast<cufftComplex*>(grid),
-                            reinterpret_cast<cufftComplex*>(grid), CUFFT_FORWARD));
+    launches += fftk::forward_object(a_eff + nn * l, a_im ? a_im + nn * l : nullptr, no, off, L, fp.tw,
+                                     grid, fp.s1, fp.s2, fp.split, s);
     dbg(s, "object_fft");
-    k_spec_mul<<<blocks_for(L2), 256, 0, s>>>(grid, fp.fringe_spec.as<float2>() + L2 * l, L2, l > 0, acc);
-    WCGH_CHECK_LAUNCH();
-    launches += 3;
+    if (fp.n_layers > 1) {  // sum_l A_l F_l, then one inverse
+      k_spec_mul<<<blocks_for(L2), 256, 0, s>>>(grid, fp.fringe_spec.as<float2>() + L2 * l, L2, l > 0,
+                                                fp.acc.as<float2>());
+      WCGH_CHECK_LAUNCH();
+      launches += 1;
+    }
   }
   dbg(s, "spec_mul");
-  WCGH_CUFFT(cufftExecC2C(fp.plan, reinterpret_cast<cufftComplex*>(acc),
-                          reinterpret_cast<cufftComplex*>(acc), CUFFT_INVERSE));
-  dbg(s, "inverse_fft");
   const PeerPlanes pp = peers ? *peers : PeerPlanes{};
-  if (nh % 2 == 0 && L % 2 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(acc) % 16 == 0 && peers_aligned16(pp))
-    k_extract2<<<blocks_for(size_t(rows) * nh / 2), 256, 0, s>>>(
-        reinterpret_cast<const float4*>(acc), L / 2, nh / 2, row0, rows, float(1.0 / double(L2)),
-        reinterpret_cast<float4*>(out), pp);
-  else
-    k_extract<<<blocks_for(size_t(rows) * nh), 256, 0, s>>>(acc, L, nh, row0, rows,
-                                                            float(1.0 / double(L2)), out, pp);
-  WCGH_CHECK_LAUNCH();
+  // one layer: the spectral product rides on the inverse's first pass
+  const bool one = fp.n_layers == 1;
+  launches += fftk::inverse_band(one ? grid : fp.acc.as<float2>(), one ? fp.fringe_spec.as<float2>() : nullptr,
+                                 L, nh, row0, rows, fp.tw, out, pp, fp.s1, fp.s2, fp.split, s);
+  dbg(s, "inverse_fft");
   if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
-  return launches + 2;
+  return launches;
 }
 
 }  // namespace wcgh

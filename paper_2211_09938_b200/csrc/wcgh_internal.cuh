@@ -320,14 +320,46 @@ int launch_expand_residual(const double* h, const double* v, const double* d, in
 
 // ---- FFT-convolution method ---------------------------------------------------
 
+// Hand-written FFTs (wcgh_fftk.cu): twiddle tables e^{-2 pi i t / len} in
+// fp64 and fp32 for len = L, L/2, L/4 (the split path's sub-rows).
+namespace fftk {
+struct Twiddles {
+  int L = 0;
+  DevBuf f32, f64;
+  void ensure(int L_, cudaStream_t s);
+  // the table of length len (L, L/2 or L/4)
+  template <typename C>
+  const C* table(int len) const {
+    const C* base;
+    if constexpr (sizeof(C) == 8) base = f32.as<C>();
+    else base = f64.as<C>();
+    size_t o = 0;  // per length: plain table (len) + stage tables (< len)
+    for (int l = L; l > len; l /= 2) o += 2 * size_t(l);
+    return base + o;
+  }
+};
+// FFT method (complex64): object / fringe spectra in the transposed layout,
+// the inverse restricted to a row band and the first nh columns (+ peers).
+// split: two scratch buffers (radix-2 pre-pass levels for rows > 8192)
+int forward_object(const float* re, const float* im, int no, int off, int L, const Twiddles& tw,
+                   float2* spec_t, DevBuf& s1, DevBuf& s2, DevBuf* split, cudaStream_t s);
+int forward_full(const float2* grid, int L, const Twiddles& tw, float2* spec_t, DevBuf& s1,
+                 DevBuf* split, cudaStream_t s);
+int inverse_band(const float2* spec_t, const float2* fringe_t, int L, int nh, int row0, int rows,
+                 const Twiddles& tw, float2* out, const PeerPlanes& peers, DevBuf& s1, DevBuf& s2,
+                 DevBuf* split, cudaStream_t s);
+// fp64 2-D DFT of an n x n field in place (natural layout), inverse unscaled.
+int fft2d_f64(double2* f, int n, bool inverse, const Twiddles& tw, DevBuf& s1, DevBuf* split,
+              cudaStream_t s);
+}  // namespace fftk
+
 struct FftPlan {
   int L = 0, n_layers = 0;
-  int plan = 0;  // cufftHandle
-  DevBuf fringe_spec, grid, acc;
+  fftk::Twiddles tw;
+  DevBuf fringe_spec, grid, acc, s1, s2, split[2];
   FftPlan() = default;
   FftPlan(const FftPlan&) = delete;
   FftPlan& operator=(const FftPlan&) = delete;
-  ~FftPlan();
 };
 // Per-layer fringe spectra on the 2Nh x 2Nh grid (precompute).
 void fft_prepare(FftPlan& fp, const wcgh_layer* layers, int n_layers, int nh, cudaStream_t stream);
@@ -340,12 +372,11 @@ int launch_fft_synthesis(FftPlan& fp, const float* a_eff, int no, int off, int n
 // ---- reconstruction and SSIM (K6, K7) --------------
 struct ReconPlan {
   int n = 0;
-  int plan = 0;  // cufftHandle (Z2Z, n x n)
-  DevBuf field;  // n x n double2 working field
+  fftk::Twiddles tw;         // fp64 tables for n
+  DevBuf field, s1, split[2];  // n x n double2 working field + FFT scratch
   ReconPlan() = default;
   ReconPlan(const ReconPlan&) = delete;
   ReconPlan& operator=(const ReconPlan&) = delete;
-  ~ReconPlan();
 };
 double2* recon_field(ReconPlan& rp, int n);
 // field <- device input (complex64 if single, else complex128)

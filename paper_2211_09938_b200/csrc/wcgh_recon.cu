@@ -5,8 +5,8 @@
 //
 //   * K6 restates build_kernel / propagate / reconstruct
 //     (angular_spectrum.cpp:11-61) and fft_2d (fft.cpp:45-68): fp64
-//     throughout like the reference. The 2-D DFTs are cuFFT Z2Z (library
-//     code, like cuBLAS); the transfer function is evaluated on the fly in
+//     throughout like the reference. The 2-D DFTs are the hand-written fp64
+//     row FFTs + transposes of wcgh_fftk.cu; the transfer function is evaluated on the fly in
 //     the spectral-product kernel (no n^2 kernel array), in the reference's
 //     operation order ((2 pi) z_signed) sqrt(s), evanescent samples zeroed;
 //     the inverse transform is scaled by 1/n^2 as fft_2d does.
@@ -18,7 +18,6 @@
 //     result is deterministic and differs from the reference only by fp64
 //     rounding.
 #include <cuda_runtime.h>
-#include <cufft.h>
 
 #include <string>
 
@@ -26,14 +25,6 @@
 
 namespace wcgh {
 namespace {
-
-#define WCGH_CUFFT(call)                                                                       \
-  do {                                                                                         \
-    cufftResult r_ = (call);                                                                   \
-    if (r_ != CUFFT_SUCCESS)                                                                   \
-      throw RuntimeError(std::string("cuFFT error ") + std::to_string(int(r_)) + " at " +     \
-                         __FILE__ + ":" + std::to_string(__LINE__));                           \
-  } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
 
@@ -165,24 +156,11 @@ __global__ void k_sum_fixed(const double* __restrict__ partial, int n, double* _
 unsigned blocks_for(size_t n, int threads) { return unsigned((n + threads - 1) / threads); }
 
 void ensure_plan(ReconPlan& rp, int n, cudaStream_t s) {
-  if (rp.plan && rp.n != n) {
-    cufftDestroy(rp.plan);
-    rp.plan = 0;
-  }
-  if (!rp.plan) {
-    cufftHandle h = 0;
-    WCGH_CUFFT(cufftPlan2d(&h, n, n, CUFFT_Z2Z));
-    rp.plan = int(h);
-    rp.n = n;
-  }
-  WCGH_CUFFT(cufftSetStream(rp.plan, s));
+  rp.tw.ensure(n, s);
+  rp.n = n;
 }
 
 }  // namespace
-
-ReconPlan::~ReconPlan() {
-  if (plan) cufftDestroy(plan);
-}
 
 double2* recon_field(ReconPlan& rp, int n) {
   return static_cast<double2*>(rp.field.reserve(sizeof(double2) * size_t(n) * n));
@@ -202,15 +180,14 @@ void load_field(ReconPlan& rp, const void* dev_in, bool single, int n, cudaStrea
 int launch_fft2d(ReconPlan& rp, int n, bool inverse, cudaStream_t s) {
   ensure_plan(rp, n, s);
   double2* f = rp.field.as<double2>();
-  WCGH_CUFFT(cufftExecZ2Z(rp.plan, reinterpret_cast<cufftDoubleComplex*>(f),
-                          reinterpret_cast<cufftDoubleComplex*>(f),
-                          inverse ? CUFFT_INVERSE : CUFFT_FORWARD));
+  int launches = fftk::fft2d_f64(f, n, inverse, rp.tw, rp.s1, rp.split, s);
   if (inverse) {
     const size_t nn = size_t(n) * n;
     k_scale<<<blocks_for(nn, 256), 256, 0, s>>>(f, nn, 1.0 / (double(n) * double(n)));
     WCGH_CHECK_LAUNCH();
+    ++launches;
   }
-  return inverse ? 2 : 1;
+  return launches;
 }
 
 int launch_transfer(int n, double wavelength, double pitch, double z_signed, double2* out,
@@ -227,18 +204,17 @@ int launch_propagate(ReconPlan& rp, int n, double wavelength, double pitch, doub
   ensure_plan(rp, n, s);
   double2* f = rp.field.as<double2>();
   const size_t nn = size_t(n) * n;
-  auto* cf = reinterpret_cast<cufftDoubleComplex*>(f);
-  WCGH_CUFFT(cufftExecZ2Z(rp.plan, cf, cf, CUFFT_FORWARD));
+  int launches = fftk::fft2d_f64(f, n, false, rp.tw, rp.s1, rp.split, s);
   k_apply_transfer<<<blocks_for(nn, 256), 256, 0, s>>>(n, 1.0 / (double(n) * pitch),
                                                         1.0 / (wavelength * wavelength), z_signed, f);
   WCGH_CHECK_LAUNCH();
-  WCGH_CUFFT(cufftExecZ2Z(rp.plan, cf, cf, CUFFT_INVERSE));
+  launches += 1 + fftk::fft2d_f64(f, n, true, rp.tw, rp.s1, rp.split, s);
   if (scaled) {  // fft_2d's 1/n^2 (reconstruct folds it into the magnitude pass)
     k_scale<<<blocks_for(nn, 256), 256, 0, s>>>(f, nn, 1.0 / (double(n) * double(n)));
     WCGH_CHECK_LAUNCH();
-    return 4;
+    ++launches;
   }
-  return 3;
+  return launches;
 }
 
 int launch_reconstruct(ReconPlan& rp, int n, double wavelength, double pitch, double z,

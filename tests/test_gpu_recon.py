@@ -84,7 +84,7 @@ def test_gpu_hologram_ssim_vs_reference_reconstruction(ctx):
     # device reconstruction of the resident plane == host round trip
     holo = job.download()
     assert np.array_equal(recon, stages.reconstruct(holo, (WL, 8e-6, 0.2)))
-    assert abs(s - O.ssim(recon, ref, 8, 0.01, 0.03, dr)) <= 1e-12
+    assert abs(s - O.ssim(recon, ref, 8, 0.01, 0.03, dr)) <= 5e-12  # two fp64 reduction orders
 
 
 # ---- test_angular_spectrum.cpp ------------------------------------------------
