@@ -494,9 +494,9 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
         rank_updates = job.stats()["updates"]
         achieved = rank_updates / (k_ms * 1e-3) if k_ms > 0 else None
     else:
-        per_clk, kernel = None, "cuFFT C2C on the 2Nh grid + k_spec_mul/k_scatter/k_extract"
-        basis = ("FFT method: the transforms are cuFFT (library); no hand-written-kernel roofline "
-                 "is claimed — `value` keeps the direct method's numerator")
+        per_clk, kernel = None, "hand-written row FFTs + transposes on the 2Nh grid (wcgh_fftk.cu)"
+        basis = ("FFT method: O(L^2 log L) hand-written Stockham row FFTs, HBM/shared-memory bound; "
+                 "no SFU/FP32 roofline applies — `value` keeps the direct method's numerator")
         bound, key = "hbm", None
         dram = int(3 * (2 * c.plane_size) ** 2 * 8 * c.n_layers + rows * c.plane_size * 8)
     peak = SM_COUNT * f_max * per_clk if per_clk else None
@@ -765,7 +765,7 @@ def alt_methods(sc, r, args, ctx, stream, flush, updates):
                 "note": ("same hologram (after_full), same numerator as `value`; "
                          + {"direct": "Eq.(1) per point x pixel on the SFU (K3)",
                             "lut": "the reference's block-LUT superposition (K4)",
-                            "fft": "correlation with the point fringe via cuFFT, O(Nh^2 log Nh)"}[alt]),
+                            "fft": "correlation with the point fringe by hand-written FFTs, O(Nh^2 log Nh)"}[alt]),
                 "algorithmic_updates": ast["updates"],
                 "precompute_ms": a_pre,
                 "rel_l2_vs_main": float(np.linalg.norm(h_alt - h_main) / np.linalg.norm(h_main)),

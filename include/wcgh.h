@@ -52,7 +52,8 @@ enum { WCGH_U8 = 0, WCGH_F32 = 1, WCGH_F64 = 2, WCGH_C128 = 3 };
  * (synthesis.cpp:18-42, 55-69) for block sizes 8/4/2/1. */
 enum { WCGH_METHOD_DIRECT = 0, WCGH_METHOD_LUT = 1, WCGH_METHOD_FFT = 2 };
 /* FFT: the same hologram as a circular correlation of A_eff with the point
- * fringe on a 2Nh x 2Nh grid (cuFFT), O(Nh^2 log Nh); SURVEY.md §8(f) row 4. */
+ * fringe on a 2Nh x 2Nh grid (hand-written FFTs, no cuFFT), O(Nh^2 log Nh);
+ * SURVEY.md §8(f) row 4. */
 
 /* Phase evaluation for DIRECT. FIXED: exact 0.64 fixed-point quadratic phase
  * frac(s * p^2/(2 lambda z)) + fp32 higher-order correction; FP64: r and

@@ -29,7 +29,7 @@
 //    CGHL payload precision) and is widened to the FringeLut's
 //    complex<double>; lut_cache_store/load go through the ABI's CGHL I/O;
 //  * build_kernel / propagate / reconstruct run in fp64 like the reference
-//    (cuFFT Z2Z); propagate evaluates the transfer function of
+//    (hand-written fp64 FFTs); propagate evaluates the transfer function of
 //    (kernel.scene, kernel.z_signed) on the device, i.e. kernel.transfer as
 //    build_kernel made it.
 #include <algorithm>

@@ -346,6 +346,110 @@ struct StBandOut {
   }
 };
 
+// ---- pipelined row FFTs (complex64, rows of 512..8192) -----------------------
+// A persistent CTA per SM walks rows r = blockIdx.x, += gridDim.x. While a
+// row's stages run, the NEXT row's raw input is already streaming into a
+// staging buffer with cp.async (no registers held), so HBM latency and
+// bandwidth overlap the shared-memory stages instead of stalling the CTA
+// (one 512-thread CTA per SM: 128 registers per thread). Staged loaders copy
+// raw bytes and build elements from them: plain rows, the spectral product
+// of two rows, the zero-padded object column block, the A_eff row.
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_bytes(char* dst, const char* src, size_t bytes, int tid, int nt) {
+  for (size_t c = size_t(tid); c < bytes / 16; c += size_t(nt)) cp16(dst + 16 * c, src + 16 * c);
+}
+
+struct PfRows {
+  const float2* p;
+  size_t stride;
+  static size_t bytes(int L, int) { return size_t(L) * 8; }
+  __device__ void prefetch(int r, char* st, int L, int tid, int nt) const {
+    cp_bytes(st, reinterpret_cast<const char*>(p + size_t(r) * stride), size_t(L) * 8, tid, nt);
+  }
+  __device__ float2 get(const char* st, int e) const { return reinterpret_cast<const float2*>(st)[e]; }
+};
+struct PfSpec {  // spectrum row (times the fringe spectrum row when f != nullptr)
+  const float2* a;
+  const float2* f;
+  size_t stride;
+  static size_t bytes(int L, int two) { return size_t(L) * 8 * (two ? 2 : 1); }
+  __device__ void prefetch(int r, char* st, int L, int tid, int nt) const {
+    cp_bytes(st, reinterpret_cast<const char*>(a + size_t(r) * stride), size_t(L) * 8, tid, nt);
+    if (f) cp_bytes(st + size_t(L) * 8, reinterpret_cast<const char*>(f + size_t(r) * stride), size_t(L) * 8, tid, nt);
+  }
+  __device__ float2 get(const char* st, int e, int L) const {
+    const float2 v = reinterpret_cast<const float2*>(st)[e];
+    if (!f) return v;
+    const float2 w = reinterpret_cast<const float2*>(st)[L + e];
+    return make_float2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+  }
+};
+struct PfPadded {  // (L x no) rows, zero-padded into [off, off + no)
+  const float2* p;
+  int no, off;
+  static size_t bytes(int, int no) { return size_t(no) * 8; }
+  __device__ void prefetch(int r, char* st, int, int tid, int nt) const {
+    cp_bytes(st, reinterpret_cast<const char*>(p + size_t(r) * no), size_t(no) * 8, tid, nt);
+  }
+  __device__ float2 get(const char* st, int e) const {
+    const int x = e - off;
+    return (x >= 0 && x < no) ? reinterpret_cast<const float2*>(st)[x] : make_float2(0.f, 0.f);
+  }
+};
+struct PfAeff {  // A_eff row r (re, optional im), zero-padded into [off, off + no)
+  const float* re;
+  const float* im;
+  int no, off;
+  static size_t bytes(int, int no) { return size_t(no) * 8; }
+  __device__ void prefetch(int r, char* st, int, int tid, int nt) const {
+    cp_bytes(st, reinterpret_cast<const char*>(re + size_t(r) * no), size_t(no) * 4, tid, nt);
+    if (im) cp_bytes(st + size_t(no) * 4, reinterpret_cast<const char*>(im + size_t(r) * no), size_t(no) * 4, tid, nt);
+  }
+  __device__ float2 get(const char* st, int e) const {
+    const int x = e - off;
+    if (x < 0 || x >= no) return make_float2(0.f, 0.f);
+    return make_float2(reinterpret_cast<const float*>(st)[x], im ? reinterpret_cast<const float*>(st)[no + x] : 0.f);
+  }
+};
+template <class Ld> __device__ __forceinline__ float2 pf_get(const Ld& ld, const char* st, int e, int) { return ld.get(st, e); }
+template <> __device__ __forceinline__ float2 pf_get<PfSpec>(const PfSpec& ld, const char* st, int e, int L) { return ld.get(st, e, L); }
+
+template <bool INV, class Ld, class St>
+__global__ void __launch_bounds__(512) k_fft_rows_pf(int L, int log2L, int rows, const float2* __restrict__ tw,
+                                                     Ld ld, St st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* F = reinterpret_cast<float2*>(smem_raw);
+  char* stg = reinterpret_cast<char*>(smem_raw) + (size_t(pad_len(L)) * 8 + 15) / 16 * 16;
+  const int t = threadIdx.x, tpr = blockDim.x;  // tpr = L / 16
+  int row = blockIdx.x;
+  if (row < rows) ld.prefetch(row, stg, L, t, tpr);
+  cp_commit();
+  for (; row < rows; row += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();  // staged row complete; previous row's stores done
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = t + i * tpr;
+      F[pad(e)] = pf_get(ld, stg, e, L);
+    }
+    __syncthreads();  // staging free: stream the next row in behind the stages
+    const int nxt = row + gridDim.x;
+    if (nxt < rows) ld.prefetch(nxt, stg, L, t, tpr);
+    cp_commit();
+    row_fft<16, INV>(F, L, log2L, t, tpr, tw);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = t + i * tpr;
+      st(row, e, F[pad(e)]);
+    }
+  }
+}
+
 // ---- transpose ------------------------------------------------------------
 template <typename C>
 __global__ void k_transpose(const C* __restrict__ in, int rows, int cols, C* __restrict__ out) {
@@ -477,14 +581,42 @@ int transpose(const C* in, int rows, int cols, C* out, cudaStream_t s) {
 
 // Object spectrum, transposed layout (L x L, row = x-frequency): the layer's
 // A_eff zero-padded into [off, off + no)^2 of the L x L grid.
+// rows of 512..8192 take the pipelined kernel, other lengths the plain one
+inline bool use_pf(int L) { return L >= 512 && L <= kMaxRowL; }
+
+template <bool INV, class Pf, class St>
+int launch_rows_pf(int L, int rows, const Twiddles& tws, Pf ld, St st, size_t stage_bytes, cudaStream_t s) {
+  const float2* tw = tws.table<float2>(L) + L;  // stage tables
+  const size_t smem = (size_t(pad_len(L)) * 8 + 15) / 16 * 16 + stage_bytes;
+  auto kern = k_fft_rows_pf<INV, Pf, St>;
+  if (smem > 48 * 1024) WCGH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0, dev = 0, sms = 0;
+  WCGH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L / 16, smem));
+  WCGH_CUDA(cudaGetDevice(&dev));
+  WCGH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::max(1, std::min(rows, std::max(1, per_sm) * sms));
+  kern<<<grid, L / 16, smem, s>>>(L, ilog2(L), rows, tw, ld, st);
+  WCGH_CHECK_LAUNCH();
+  return 1;
+}
+
 int forward_object(const float* re, const float* im, int no, int off, int L, const Twiddles& tw,
                    float2* spec_t, DevBuf& s1, DevBuf& s2, DevBuf* split, cudaStream_t s) {
   float2* rowsft = static_cast<float2*>(s1.reserve(sizeof(float2) * size_t(no) * L));
   float2* tr = static_cast<float2*>(s2.reserve(sizeof(float2) * size_t(no) * L));
-  int n = fft_rows<float2, false>(L, no, tw, LdAeffRow{re, im, no, off}, StRows<float2>{rowsft, size_t(L)},
-                                  split, s);
+  int n = 0;
+  if (use_pf(L) && no % 4 == 0)
+    n += launch_rows_pf<false>(L, no, tw, PfAeff{re, im, no, off}, StRows<float2>{rowsft, size_t(L)},
+                               size_t(no) * 8, s);
+  else
+    n += fft_rows<float2, false>(L, no, tw, LdAeffRow{re, im, no, off}, StRows<float2>{rowsft, size_t(L)},
+                                 split, s);
   n += transpose(rowsft, no, L, tr, s);  // (no x L) -> (L x no)
-  n += fft_rows<float2, false>(L, L, tw, LdPadded{tr, no, off}, StRows<float2>{spec_t, size_t(L)}, split, s);
+  if (use_pf(L) && no % 2 == 0)
+    n += launch_rows_pf<false>(L, L, tw, PfPadded{tr, no, off}, StRows<float2>{spec_t, size_t(L)},
+                               size_t(no) * 8, s);
+  else
+    n += fft_rows<float2, false>(L, L, tw, LdPadded{tr, no, off}, StRows<float2>{spec_t, size_t(L)}, split, s);
   return n;
 }
 
@@ -507,12 +639,21 @@ int inverse_band(const float2* spec_t, const float2* fringe_t, int L, int nh, in
                  DevBuf* split, cudaStream_t s) {
   float2* g = static_cast<float2*>(s1.reserve(sizeof(float2) * size_t(L) * rows));
   float2* gt = static_cast<float2*>(s2.reserve(sizeof(float2) * size_t(L) * rows));
-  int n = fft_rows<float2, true>(L, L, tw, LdSpec{spec_t, fringe_t, size_t(L)}, StBandRows{g, row0, rows},
-                                 split, s);
+  int n = 0;
+  if (use_pf(L))
+    n += launch_rows_pf<true>(L, L, tw, PfSpec{spec_t, fringe_t, size_t(L)}, StBandRows{g, row0, rows},
+                              size_t(L) * 8 * (fringe_t ? 2 : 1), s);
+  else
+    n += fft_rows<float2, true>(L, L, tw, LdSpec{spec_t, fringe_t, size_t(L)}, StBandRows{g, row0, rows},
+                                split, s);
   n += transpose(g, L, rows, gt, s);  // (L x rows) -> (rows x L)
   const float scale = float(1.0 / (double(L) * double(L)));
-  n += fft_rows<float2, true>(L, rows, tw, LdRows<float2>{gt, size_t(L)}, StBandOut{out, nh, scale, peers},
-                              split, s);
+  if (use_pf(L))
+    n += launch_rows_pf<true>(L, rows, tw, PfRows{gt, size_t(L)}, StBandOut{out, nh, scale, peers},
+                              size_t(L) * 8, s);
+  else
+    n += fft_rows<float2, true>(L, rows, tw, LdRows<float2>{gt, size_t(L)}, StBandOut{out, nh, scale, peers},
+                                split, s);
   return n;
 }
 
