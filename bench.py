@@ -331,23 +331,36 @@ class ReferenceTimer:
 
 
 def reference_direct_rate():
-    """The reference's own direct Eq.(1) (pointwise_hologram_reference,
-    tests/support/oracles.cpp:12-36 — the formula K3 evaluates), single
-    thread, on a seeded 64^2 object: updates/s (SURVEY.md §8(d) direct-formula
-    baseline)."""
+    """SURVEY.md §8(d)'s two further CPU baselines, on BASELINE config 0
+    (128^2 blob object, z 0.2 m, pitch 8 um), whole holograms: the
+    reference's own direct Eq.(1) (pointwise_hologram_reference,
+    tests/support/oracles.cpp:12-36 — the formula K3 evaluates; single
+    thread) and its production point-wise hologram synthesize_pointwise_oracle
+    (synthesis.cpp:255-286: the B = 1 LUT at every pixel, workers = nproc; its
+    LUT build excluded). updates = nonzero object pixels x plane pixels."""
     from oracle import oracle as O
+    from paper_2211_09938_b200 import scenes
 
     if not O.ref_available():
         return None
-    n = 64
-    amp = np.random.default_rng(64).random((n, n))
+    sc = scenes.make_scene(0)
+    obj = sc.objects[0].astype(np.float64)
+    n = obj.shape[0]
+    upd = float(np.count_nonzero(obj)) * n * n
     t0 = time.perf_counter()
-    O.ref_pointwise_hologram_reference(amp, 532e-9, 8e-6, 0.2)
+    O.ref_pointwise_hologram_reference(obj, 532e-9, 8e-6, 0.2)
     dt = time.perf_counter() - t0
-    upd = float(np.count_nonzero(amp)) * n * n
-    return {"value": upd / dt, "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"pointwise_hologram_reference on a {n}^2 object / {n}^2 plane, 1 thread, "
-                      f"{dt:.2f} s", **host_cpu()}
+    direct = {"value": upd / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+              "sample": f"pointwise_hologram_reference, whole config-0 hologram ({n}^2), 1 thread, "
+                        f"{dt:.2f} s", **host_cpu()}
+    t0 = time.perf_counter()
+    O.ref_pointwise_oracle(obj, 532e-9, 8e-6, 0.2, workers=0)
+    dt2 = time.perf_counter() - t0
+    direct["pointwise_oracle"] = {
+        "value": upd / dt2, "unit": UNIT, "cores": O.ref_default_workers(), "kind": "reference",
+        "sample": (f"synthesize_pointwise_oracle, whole config-0 hologram ({n}^2, B=1 LUT built "
+                   f"inside the timed call), {dt2:.3f} s")}
+    return direct
 
 
 def reference_cpu_sample(scene, budget_s: float = 10.0):
@@ -518,6 +531,8 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
     }
     if traffic_src:
         roof["traffic_source"] = traffic_src
+        n_launch = max(1, (job.stats().get("synth_launches") or 1))
+        roof["achieved_dram_gbs"] = traffic * n_launch / (k_ms * 1e-3) / 1e9 if k_ms > 0 else None
         roof["traffic_note"] = ("dram__bytes_read+write per K3/K4 launch from one `ncu --set full` "
                                 "capture; dominated by the fixed-order fp32 partial-sum planes "
                                 "(compute-bound kernel, < 1% DRAM utilisation)")

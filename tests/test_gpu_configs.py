@@ -77,7 +77,8 @@ def _full_plane_check(cfg, frac, method):
     assert err <= REL_L2, (cfg, frac, method, err)
     s = _ssim_vs(holo, ref_rec, (c.wavelength, c.pitch, c.depths[0]))
     _record(test="full_plane_vs_fft_oracle", cfg=cfg, saliency_frac=frac, method=method,
-            rel_l2=err, ssim=s, n_points=st["n_points"], ops=st["ops"])
+            rel_l2=err, max_rel_error=O.max_rel_error(holo, ref), ssim=s, n_points=st["n_points"],
+            ops=st["ops"])
     assert s >= SSIM_MIN, (cfg, frac, method, s)
     job.close()
     return err, s
@@ -120,7 +121,8 @@ def test_cfg1_full_plane_vs_reference(ctx, method):
     snaps = job.download_stages()
     stage_err = [O.rel_l2(snaps[s], planes[s]) for s in range(4)]
     _record(test="cfg1_vs_reference_synthesize_progressive", cfg=1, method=method, rel_l2=err,
-            ssim=ssim, stage_rel_l2=stage_err, ops=st["ops"], ref_ops=ops.tolist())
+            max_rel_error=O.max_rel_error(holo, planes[3]), ssim=ssim, stage_rel_l2=stage_err,
+            ops=st["ops"], ref_ops=ops.tolist())
     assert err <= REL_L2, err
     assert ssim >= SSIM_MIN
     for s in range(4):
