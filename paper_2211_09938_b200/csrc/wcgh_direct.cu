@@ -203,6 +203,225 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Recurrence form of the fixed-point kernel (P = 32): a thread owns 32
+// CONSECUTIVE pixels of its row as two runs A = [x0, x0+16), B = [x0+16,
+// x0+32), processed as the two lanes of packed fp32x2 arithmetic. For one
+// point, each run is seeded exactly at its first pixel and then advanced by
+// angle addition:
+//   w_0 = a(x0) e^{i phi(x0)}                      (fixed-point phase, 2 MUFU)
+//   v_0 = a(x0+1)/a(x0) e^{i (phi(x0+1)-phi(x0))}  (first difference)
+//   w_{i+1} = w_i v_i,  v_{i+1} = v_i (1 + sigma)  (sigma: second difference)
+// so a pixel costs two complex multiplies and one complex add (10 lane
+// operations, 5 packed instructions) instead of two MUFU.
+// * The quadratic part of the first difference, alpha (2 dx + 1) cycles, is
+//   exact 0.32 fixed point; its top 6 bits index a 64-entry table of
+//   e^{2 pi i k/64} (fp64-rounded) and the remaining angle (|x| <= pi/64 plus
+//   the correction's first difference, at most a few 1e-3 rad) goes through
+//   short odd/even polynomials (truncation < 1e-10), so v_0 carries no MUFU
+//   error into the run (a seed error grows linearly along it).
+// * The correction and log-amplitude first differences are the midpoint
+//   derivatives (error O(du^3)); the second difference is evaluated at the
+//   run's middle, so the neglected third difference contributes at most
+//   L^3/12 * phi''' (<= 1.2e-6 rad at the config-4 corner).
+// * sigma = e^{l2 + i delta} - 1 to third order in delta; it is applied as
+//   v + v sigma (sigma ~ 1e-3), so its own rounding is relative to sigma.
+// Accumulated fp32 rounding along a 16-pixel run: ~1e-6 rad at its end.
+// The summation order (points in chunk order, chunks reduced in order) is
+// the fixed kernel's, so band invariance is unchanged.
+template <int NC, int AMP, int MINB, bool CPLX>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_direct_rec(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
+                 int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
+                 int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
+  constexpr int L = 16;  // run length; 2 runs per thread
+  __shared__ int4 sp[kBatch];
+  __shared__ float s_tr[64], s_ti[64];
+  if (threadIdx.x < 64) {
+    double sn, cs;
+    sincospi(double(threadIdx.x) / 32.0, &sn, &cs);
+    s_tr[threadIdx.x] = float(cs);
+    s_ti[threadIdx.x] = float(sn);
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int tx = blockIdx.x % tiles_x;
+  const int ty = blockIdx.x / tiles_x;
+  const int row = ty * 8 + warp;
+  const int y = row0 + row;
+  const int x0 = tx * 1024 + 32 * lane;
+  const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
+  const long long p1 = min(p0 + kChunk, n_points);
+
+  // hr[i] = (re of pixel x0 + i, re of pixel x0 + L + i); hi likewise
+  float2 hr[L], hi[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) hr[i] = hi[i] = make_float2(0.0f, 0.0f);
+
+  for (int l = 0; l < n_layers; ++l) {
+    long long s0, s1;
+    layer_span(layer_begin, l, p0, p1, s0, s1);
+    if (s0 >= s1) continue;
+    const DirectLayer& Ly = c_layers[l];
+    const uint32_t a_hi = Ly.a_hi, a_lo = Ly.a_lo, phi0 = Ly.phi0;
+    const float c = Ly.c, inv_z = Ly.inv_z;
+    float2 corr[NC], dcorr[NC], ddcorr[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      corr[k] = make_float2(Ly.corr[k], Ly.corr[k]);
+      dcorr[k] = make_float2(Ly.dcorr[k], Ly.dcorr[k]);
+      ddcorr[k] = make_float2(Ly.ddcorr[k], Ly.ddcorr[k]);
+    }
+    const float am1 = Ly.amp[0], am2 = Ly.amp[1], am3 = Ly.amp[2];
+    const float2 two_pi2 = make_float2(kTwoPi, kTwoPi);
+    const float2 neg3pi2 = make_float2(kNegThreePi, kNegThreePi);
+    const float2 c2 = make_float2(2.0f * c, 2.0f * c), cc = make_float2(c, c);
+    const float2 half2 = make_float2(0.5f, 0.5f), nhalf2 = make_float2(-0.5f, -0.5f);
+    const float2 cmid_a = make_float2(c * float(L - 1), c * float(L - 1));
+    const float2 cmid_b = make_float2(c * (float(L * L) * 0.25f - 0.5f), c * (float(L * L) * 0.25f - 0.5f));
+    const float2 cL = make_float2(c * float(L), c * float(L));
+    const float2 dq2 = make_float2(Ly.dq, Ly.dq), lc2 = make_float2(-c, -c);
+    const float2 xscale = make_float2(kTwoPi / 536870912.0f, kTwoPi / 536870912.0f);  // 2pi / 2^29
+    const float2 s3 = make_float2(-1.0f / 6.0f, -1.0f / 6.0f), s5 = make_float2(1.0f / 120.0f, 1.0f / 120.0f);
+    const float2 c4 = make_float2(1.0f / 24.0f, 1.0f / 24.0f);
+
+    for (long long b = s0; b < s1; b += kBatch) {
+      const int nb = int(min((long long)kBatch, s1 - b));
+      __syncthreads();
+      for (int i = threadIdx.x; i < nb; i += kThreads) {
+        WCGH_DCHECK(b + i < n_points && b + i >= 0);
+        sp[i] = pts[b + i];
+      }
+      __syncthreads();
+
+#pragma unroll 1
+      for (int j = 0; j < nb; ++j) {
+        const int4 q = sp[j];
+        const int dxa = x0 - q.x, dxb = dxa + L;
+        const int dy = y - q.y;
+        const int dy2 = dy * dy;
+        const uint32_t ph0 = CPLX ? phi0 + uint32_t(q.w) : phi0;
+        const uint32_t sa = uint32_t(dxa * dxa + dy2), sb = uint32_t(dxb * dxb + dy2);
+        const uint32_t ta = sa * a_hi + __umulhi(sa, a_lo) + ph0;
+        const uint32_t tb = sb * a_hi + __umulhi(sb, a_lo) + ph0;
+        // first difference of the quadratic phase: frac(alpha (2 dx + 1)), exact
+        const int ma = 2 * dxa + 1, mb = ma + 2 * L;
+        const uint32_t da = uint32_t(ma) * a_hi + uint32_t(((long long)ma * (long long)a_lo) >> 32);
+        const uint32_t db = uint32_t(mb) * a_hi + uint32_t(((long long)mb * (long long)a_lo) >> 32);
+
+        const float2 fx = make_float2(i2f_small(dxa), i2f_small(dxb));
+        const float fdy = i2f_small(dy);
+        const float uy = fdy * fdy * c;
+        const float2 U = __ffma2_rn(__fmul2_rn(fx, cc), fx, make_float2(uy, uy));
+
+        // ---- seed w_0 (the fixed kernel's per-pixel evaluation)
+        float2 wr, wi;
+        {
+          const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
+                                         __int_as_float((tb >> 9) | 0x3f800000u));
+          const float2 u2 = __fmul2_rn(U, U);
+          float2 pc = corr[NC - 1];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
+          const float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
+          const float a0 = __int_as_float(q.z) * inv_z;
+          const float2 A0 = make_float2(a0, a0);
+          float2 am;
+          if constexpr (AMP == 3) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2),
+                         A3 = make_float2(a0 * am3, a0 * am3);
+            am = __ffma2_rn(__ffma2_rn(__ffma2_rn(A3, U, A2), U, A1), U, A0);
+          } else if constexpr (AMP == 2) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2);
+            am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
+          } else if constexpr (AMP == 1) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1);
+            am = __ffma2_rn(A1, U, A0);
+          } else {
+            am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
+          }
+          float2 sn, cs;
+          __sincosf(ph.x, &sn.x, &cs.x);
+          __sincosf(ph.y, &sn.y, &cs.y);
+          wr = __fmul2_rn(am, cs);
+          wi = __fmul2_rn(am, sn);
+        }
+
+        // ---- seed v_0 and sigma
+        float2 vr, vi, sr, si;
+        {
+          const float2 du = __ffma2_rn(fx, c2, cc);      // u(x+1) - u(x) = c (2x + 1)
+          const float2 um = __ffma2_rn(du, half2, U);    // u at x + 1/2
+          float2 gq = dcorr[NC - 1], gpp = ddcorr[NC - 1];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) {
+            gq = __ffma2_rn(gq, um, dcorr[k]);
+            gpp = __ffma2_rn(gpp, um, ddcorr[k]);
+          }
+          const float2 gp = __fmul2_rn(gq, um);          // G h'(um), radians per unit u
+          const float2 dc = __fmul2_rn(du, gp);          // correction's first difference
+          const float2 l0 = __fmul2_rn(du, __ffma2_rn(um, half2, nhalf2));  // ln a(x+1) - ln a(x)
+          // quadratic part: table entry k = round(D / 2^26) and the remainder
+          const uint32_t ea = da + (1u << 25), eb = db + (1u << 25);
+          const float2 xr = make_float2(
+              __int_as_float(0x4b000000u | ((ea & 0x3ffffffu) >> 3)) - 12582912.0f,
+              __int_as_float(0x4b000000u | ((eb & 0x3ffffffu) >> 3)) - 12582912.0f);
+          const float2 X = __ffma2_rn(xr, xscale, dc);   // |X| <= pi/64 + |dc|
+          const float2 X2 = __fmul2_rn(X, X);
+          const float2 sx = __ffma2_rn(X, __fmul2_rn(X2, __ffma2_rn(X2, s5, s3)), X);  // sin X
+          const float2 cx = __fmul2_rn(X2, __ffma2_rn(X2, c4, nhalf2));               // cos X - 1
+          const float2 cr = __fadd2_rn(cx, l0);          // e^{l0} e^{iX} - 1, real part
+          const float2 ci = __ffma2_rn(sx, l0, sx);      //                   imaginary part
+          const int ka = int(ea >> 26), kb = int(eb >> 26);
+          const float2 tr = make_float2(s_tr[ka], s_tr[kb]), ti = make_float2(s_ti[ka], s_ti[kb]);
+          const float2 t0 = __ffma2_rn(ti, ci, make_float2(-tr.x, -tr.y));  // ti ci - tr
+          vr = __ffma2_rn(tr, cr, make_float2(-t0.x, -t0.y));               // tr (1 + cr) - ti ci
+          vi = __ffma2_rn(ti, cr, __ffma2_rn(tr, ci, ti));                  // ti (1 + cr) + tr ci
+          // second difference at the run's middle x + L/2
+          const float2 dmu = __ffma2_rn(fx, cmid_a, cmid_b);  // u(x + L/2) - um
+          const float2 gpm = __ffma2_rn(gpp, dmu, gp);        // G h'(u(x + L/2))
+          const float2 upm = __ffma2_rn(fx, c2, cL);          // u'(x + L/2) = 2c (x + L/2)
+          const float2 dl = __ffma2_rn(gpp, __fmul2_rn(upm, upm), __ffma2_rn(gpm, c2, dq2));
+          const float2 dl2 = __fmul2_rn(dl, dl);
+          sr = __ffma2_rn(dl2, nhalf2, lc2);                  // l2 - delta^2/2
+          si = __ffma2_rn(dl, __fmul2_rn(dl2, s3), dl);       // delta - delta^3/6
+        }
+
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          hr[i] = __fadd2_rn(hr[i], wr);
+          hi[i] = __fadd2_rn(hi[i], wi);
+          if (i < L - 1) {
+            const float2 t1 = __fmul2_rn(wi, vi), t2 = __fmul2_rn(wi, vr);
+            const float2 nwr = __ffma2_rn(wr, vr, make_float2(-t1.x, -t1.y));
+            wi = __ffma2_rn(wr, vi, t2);
+            wr = nwr;
+            const float2 ta2 = __ffma2_rn(vi, si, make_float2(-vr.x, -vr.y));  // vi si - vr
+            const float2 tb2 = __ffma2_rn(vr, si, vi);                          // vi + vr si
+            vr = __ffma2_rn(vr, sr, make_float2(-ta2.x, -ta2.y));
+            vi = __ffma2_rn(vi, sr, tb2);
+          }
+        }
+      }
+    }
+  }
+
+  if (row < rows) {
+    float2* dst = out + blockIdx.y * out_chunk_stride + size_t(row) * nh;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int p = 2 * m, x = x0 + p;
+      const float4 r = p < L ? make_float4(hr[p].x, hi[p].x, hr[p + 1].x, hi[p + 1].x)
+                             : make_float4(hr[p - L].y, hi[p - L].y, hr[p - L + 1].y, hi[p - L + 1].y);
+      WCGH_DCHECK(x >= nh || size_t(blockIdx.y) * out_chunk_stride + size_t(row) * nh + x <
+                                 size_t(gridDim.y) * out_chunk_stride);
+      if (x + 1 < nh)
+        *reinterpret_cast<float4*>(dst + x) = r;
+      else if (x < nh)
+        dst[x] = make_float2(r.x, r.y);
+    }
+  }
+}
+
 // Double-phase option: r and k*r in fp64, reduced to [-pi, pi] in fp64, then
 // fp32 sin/cos. Accuracy mode (FP64-pipe bound).
 template <int P>
@@ -336,6 +555,40 @@ struct LaunchArgs {
   size_t stride;
 };
 
+template <int NC, int AMP>
+void launch_rec(const LaunchArgs& a) {
+  constexpr int MINB = 2;
+  if (a.cplx)
+    k_direct_rec<NC, AMP, MINB, true><<<a.grid, kThreads, 0, a.s>>>(
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+  else
+    k_direct_rec<NC, AMP, MINB, false><<<a.grid, kThreads, 0, a.s>>>(
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+}
+
+template <int NC>
+void launch_rec_amp(const DirectPlan& plan, const LaunchArgs& a) {
+  if (plan.amp_degree == 1)
+    launch_rec<NC, 1>(a);
+  else if (plan.amp_degree == 2)
+    launch_rec<NC, 2>(a);
+  else if (plan.amp_degree == 3)
+    launch_rec<NC, 3>(a);
+  else
+    launch_rec<NC, 0>(a);
+}
+
+void launch_rec_nc(const DirectPlan& plan, const LaunchArgs& a) {
+  if (plan.n_corr <= 2)
+    launch_rec_amp<2>(plan, a);
+  else if (plan.n_corr <= 3)
+    launch_rec_amp<3>(plan, a);
+  else if (plan.n_corr <= 5)
+    launch_rec_amp<5>(plan, a);
+  else
+    launch_rec_amp<8>(plan, a);
+}
+
 template <int P, int NC, int AMP>
 void launch_fixed(const LaunchArgs& a) {
   constexpr int MINB = 2;
@@ -404,6 +657,15 @@ DirectLayer make_direct_layer(const wcgh_layer& L) {
   const double two_pi = 6.283185307179586476925286766559;
   for (int k = 0; k < kMaxCorr; ++k) d.corr[k] = float(two_pi * K * binom(0.5, k + 2));
   for (int k = 0; k < 4; ++k) d.amp[k] = float(binom(-0.5, k + 1));
+  for (int k = 0; k < kMaxCorr; ++k) {
+    const double ck = two_pi * K * binom(0.5, k + 2);
+    d.dcorr[k] = float((k + 2) * ck);
+    d.ddcorr[k] = float((k + 2) * (k + 1) * ck);
+  }
+  // second difference of the quadratic phase between adjacent pixels: 2 alpha
+  // cycles, centred (the recurrence rotates by it each step)
+  const double f2 = 2.0 * alpha - std::nearbyint(2.0 * alpha);
+  d.dq = float(two_pi * f2);
   d.wavelength = lam;
   d.pitch = p;
   d.z = z;
@@ -479,9 +741,23 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     return 0;
   }
   DirectPlan plan{};
-  if (phase_mode == WCGH_PHASE_FIXED) plan = plan_direct(layers, n_layers, max_dx, max_dy);
   DirectLayer h_layers[kMaxLayers];
   for (int l = 0; l < n_layers; ++l) h_layers[l] = make_direct_layer(layers[l]);
+  if (phase_mode == WCGH_PHASE_FIXED) {
+    plan = plan_direct(layers, n_layers, max_dx, max_dy);
+    // the recurrence form: 32 consecutive pixels per thread (P = 32, float4
+    // stores need an even width), small per-pixel rotation of the quadratic
+    // phase and a small u (the series of sigma and of the log-amplitude
+    // differences, see k_direct_rec). WCGH_DIRECT_REC=0 forces the per-pixel
+    // evaluation (k_direct_fixed) for comparisons.
+    static const int rec_env = [] {
+      const char* e = std::getenv("WCGH_DIRECT_REC");
+      return e ? std::atoi(e) : 1;
+    }();
+    bool rec = rec_env != 0 && pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02;
+    for (int l = 0; l < n_layers; ++l) rec = rec && std::fabs(h_layers[l].dq) <= 0.03f;
+    plan.rec = rec;
+  }
   WCGH_CUDA(cudaMemcpyToSymbolAsync(c_layers, h_layers, sizeof(DirectLayer) * n_layers, 0,
                                     cudaMemcpyHostToDevice, stream));
 
@@ -521,7 +797,9 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
       else
         k_direct_fp64<4><<<a.grid, kThreads, 0, stream>>>(a.pts, a.cplx, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
     } else {
-      if (P == 32)
+      if (P == 32 && plan.rec)
+        launch_rec_nc(plan, a);
+      else if (P == 32)
         launch_fixed_nc<32>(plan, a);
       else if (P == 16)
         launch_fixed_nc<16>(plan, a);

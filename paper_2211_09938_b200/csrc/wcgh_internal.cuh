@@ -177,6 +177,12 @@ struct DirectLayer {
   float inv_z;           // 1/z
   float corr[kMaxCorr];  // 2*pi*(z/lambda)*C(1/2, n+2): radians per u^(n+2)
   float amp[4];          // C(-1/2, n+1): (1+u)^(-1/2) = 1 + sum amp[n] u^(n+1)
+  // recurrence form (k_direct_rec): derivatives of the correction series,
+  // d/du: sum dcorr[n] u^(n+1), d2/du2: sum ddcorr[n] u^n (radians), and the
+  // quadratic phase's second difference between adjacent pixels, 2 alpha
+  // cycles, centred and in radians.
+  float dcorr[kMaxCorr], ddcorr[kMaxCorr];
+  float dq;
   double wavelength, pitch, z, k;  // fp64 phase mode
 };
 
@@ -184,6 +190,7 @@ struct DirectPlan {
   int n_corr;      // phase-series terms used (2, 3, 5 or 8)
   int amp_degree;  // (1+u)^(-1/2): polynomial degree 1, 2 or 3, or 0 = MUFU.RSQ
   double u_max;
+  bool rec;        // angle-addition recurrence along 16-pixel runs (k_direct_rec)
 };
 
 // CUDA-event pairs around each launch of a kernel family (for per-kernel
