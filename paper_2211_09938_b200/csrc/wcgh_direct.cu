@@ -214,34 +214,39 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // so a pixel costs two complex multiplies and one complex add (10 lane
 // operations, 5 packed instructions) instead of two MUFU.
 // * The quadratic part of the first difference, alpha (2 dx + 1) cycles, is
-//   exact 0.32 fixed point; its top 6 bits index a 64-entry table of
-//   e^{2 pi i k/64} (fp64-rounded) and the remaining angle (|x| <= pi/64 plus
-//   the correction's first difference, at most a few 1e-3 rad) goes through
-//   short odd/even polynomials (truncation < 1e-10), so v_0 carries no MUFU
-//   error into the run (a seed error grows linearly along it).
+//   exact 0.32 fixed point; its top 8 bits index a 256-entry table of
+//   e^{2 pi i k/256} (fp64-rounded) and the remaining angle (|x| <= pi/256
+//   plus the correction's first difference, <= 0.024 rad at config 4) goes
+//   through sin x = x - x^3/6, cos x - 1 = -x^2/2 (truncation <= 1.2e-8), so
+//   v_0 carries no MUFU error into the run (a seed error grows linearly).
+// * Run B's fixed-point phase and first difference follow from run A's by
+//   exact integer identities (t_B = t_A + L D_A + alpha L(L-1), D_B = D_A +
+//   2 L alpha), so only run A pays the 64-bit products.
 // * The correction and log-amplitude first differences are the midpoint
 //   derivatives (error O(du^3)); the second difference is evaluated at the
 //   run's middle, so the neglected third difference contributes at most
 //   L^3/12 * phi''' (<= 1.2e-6 rad at the config-4 corner).
-// * sigma = e^{l2 + i delta} - 1 to third order in delta; it is applied as
-//   v + v sigma (sigma ~ 1e-3), so its own rounding is relative to sigma.
+// * sigma = e^{l2 + i delta} - 1 to third order in delta (the cubic term of
+//   the quadratic part folded into a constant); it is applied as v + v sigma
+//   (sigma ~ 1e-3), so its own rounding is relative to sigma.
 // Accumulated fp32 rounding along a 16-pixel run: ~1e-6 rad at its end.
 // The summation order (points in chunk order, chunks reduced in order) is
 // the fixed kernel's, so band invariance is unchanged.
-template <int NC, int AMP, int MINB, bool CPLX>
+template <int NC, int AMP, int MINB, bool CPLX, int RU>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_direct_rec(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
                  int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
                  int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
   constexpr int L = 16;  // run length; 2 runs per thread
   __shared__ int4 sp[kBatch];
-  __shared__ float s_tr[64], s_ti[64];
-  if (threadIdx.x < 64) {
+  __shared__ float s_tr[256], s_ti[256];
+  {
     double sn, cs;
-    sincospi(double(threadIdx.x) / 32.0, &sn, &cs);
+    sincospi(double(threadIdx.x) / 128.0, &sn, &cs);
     s_tr[threadIdx.x] = float(cs);
     s_ti[threadIdx.x] = float(sn);
   }
+  static_assert(kThreads == 256, "one table entry per thread");
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int tx = blockIdx.x % tiles_x;
@@ -263,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (s0 >= s1) continue;
     const DirectLayer& Ly = c_layers[l];
     const uint32_t a_hi = Ly.a_hi, a_lo = Ly.a_lo, phi0 = Ly.phi0;
+    const uint32_t t_ab = Ly.t_ab, d_ab = Ly.d_ab;
     const float c = Ly.c, inv_z = Ly.inv_z;
     float2 corr[NC], dcorr[NC], ddcorr[NC];
 #pragma unroll
@@ -279,39 +285,43 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const float2 cmid_a = make_float2(c * float(L - 1), c * float(L - 1));
     const float2 cmid_b = make_float2(c * (float(L * L) * 0.25f - 0.5f), c * (float(L * L) * 0.25f - 0.5f));
     const float2 cL = make_float2(c * float(L), c * float(L));
-    const float2 dq2 = make_float2(Ly.dq, Ly.dq), lc2 = make_float2(-c, -c);
-    const float2 xscale = make_float2(kTwoPi / 536870912.0f, kTwoPi / 536870912.0f);  // 2pi / 2^29
-    const float2 s3 = make_float2(-1.0f / 6.0f, -1.0f / 6.0f), s5 = make_float2(1.0f / 120.0f, 1.0f / 120.0f);
-    const float2 c4 = make_float2(1.0f / 24.0f, 1.0f / 24.0f);
+    const float2 dq3 = make_float2(Ly.dq3, Ly.dq3), ndq = make_float2(-Ly.dq, -Ly.dq);
+    const float2 sr0 = make_float2(Ly.sr0, Ly.sr0);
+    const float2 xscale = make_float2(kTwoPi / 2147483648.0f, kTwoPi / 2147483648.0f);  // 2pi / 2^31
+    const float2 s3 = make_float2(-1.0f / 6.0f, -1.0f / 6.0f);
 
     for (long long b = s0; b < s1; b += kBatch) {
       const int nb = int(min((long long)kBatch, s1 - b));
       __syncthreads();
       for (int i = threadIdx.x; i < nb; i += kThreads) {
         WCGH_DCHECK(b + i < n_points && b + i >= 0);
-        sp[i] = pts[b + i];
+        int4 r = pts[b + i];
+        // real amplitudes: stage a0 = A/z and a0 * am1 once per CTA instead
+        // of once per thread (complex records keep their phase in .w)
+        const float a0 = __int_as_float(r.z) * inv_z;
+        r.z = __float_as_int(a0);
+        if (!CPLX) r.w = __float_as_int(a0 * am1);
+        sp[i] = r;
       }
       __syncthreads();
 
-#pragma unroll 1
+#pragma unroll RU
       for (int j = 0; j < nb; ++j) {
         const int4 q = sp[j];
-        const int dxa = x0 - q.x, dxb = dxa + L;
+        const int dxa = x0 - q.x;
         const int dy = y - q.y;
-        const int dy2 = dy * dy;
         const uint32_t ph0 = CPLX ? phi0 + uint32_t(q.w) : phi0;
-        const uint32_t sa = uint32_t(dxa * dxa + dy2), sb = uint32_t(dxb * dxb + dy2);
-        const uint32_t ta = sa * a_hi + __umulhi(sa, a_lo) + ph0;
-        const uint32_t tb = sb * a_hi + __umulhi(sb, a_lo) + ph0;
+        const int sa = dxa * dxa + dy * dy;
+        const int sb = sa + (2 * L) * dxa + L * L;
+        const uint32_t ta = uint32_t(sa) * a_hi + __umulhi(uint32_t(sa), a_lo) + ph0;
         // first difference of the quadratic phase: frac(alpha (2 dx + 1)), exact
-        const int ma = 2 * dxa + 1, mb = ma + 2 * L;
+        const int ma = 2 * dxa + 1;
         const uint32_t da = uint32_t(ma) * a_hi + uint32_t(((long long)ma * (long long)a_lo) >> 32);
-        const uint32_t db = uint32_t(mb) * a_hi + uint32_t(((long long)mb * (long long)a_lo) >> 32);
+        const uint32_t tb = ta + (da << 4) + t_ab;  // L = 16
+        const uint32_t db = da + d_ab;
 
-        const float2 fx = make_float2(i2f_small(dxa), i2f_small(dxb));
-        const float fdy = i2f_small(dy);
-        const float uy = fdy * fdy * c;
-        const float2 U = __ffma2_rn(__fmul2_rn(fx, cc), fx, make_float2(uy, uy));
+        const float2 fx = make_float2(i2f_small(dxa), i2f_small(dxa + L));
+        const float2 U = __fmul2_rn(make_float2(__int2float_rn(sa), __int2float_rn(sb)), cc);
 
         // ---- seed w_0 (the fixed kernel's per-pixel evaluation)
         float2 wr, wi;
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
           for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
           const float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
-          const float a0 = __int_as_float(q.z) * inv_z;
+          const float a0 = __int_as_float(q.z);
           const float2 A0 = make_float2(a0, a0);
           float2 am;
           if constexpr (AMP == 3) {
@@ -334,8 +344,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2);
             am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
           } else if constexpr (AMP == 1) {
-            const float2 A1 = make_float2(a0 * am1, a0 * am1);
-            am = __ffma2_rn(A1, U, A0);
+            const float a1 = CPLX ? a0 * am1 : __int_as_float(q.w);
+            am = __ffma2_rn(make_float2(a1, a1), U, A0);
           } else {
             am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
           }
@@ -358,20 +368,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
             gpp = __ffma2_rn(gpp, um, ddcorr[k]);
           }
           const float2 gp = __fmul2_rn(gq, um);          // G h'(um), radians per unit u
-          const float2 dc = __fmul2_rn(du, gp);          // correction's first difference
-          const float2 l0 = __fmul2_rn(du, __ffma2_rn(um, half2, nhalf2));  // ln a(x+1) - ln a(x)
-          // quadratic part: table entry k = round(D / 2^26) and the remainder
-          const uint32_t ea = da + (1u << 25), eb = db + (1u << 25);
+          const float2 l0 = __fmul2_rn(du, nhalf2);      // ln a(x+1) - ln a(x) = -du/2 (1 - O(u))
+          // quadratic part: table entry k = round(D / 2^24) and the remainder
+          const uint32_t ea = da + (1u << 23), eb = db + (1u << 23);
           const float2 xr = make_float2(
-              __int_as_float(0x4b000000u | ((ea & 0x3ffffffu) >> 3)) - 12582912.0f,
-              __int_as_float(0x4b000000u | ((eb & 0x3ffffffu) >> 3)) - 12582912.0f);
-          const float2 X = __ffma2_rn(xr, xscale, dc);   // |X| <= pi/64 + |dc|
+              __int_as_float(0x4b000000u | ((ea & 0xffffffu) >> 1)) - 12582912.0f,
+              __int_as_float(0x4b000000u | ((eb & 0xffffffu) >> 1)) - 12582912.0f);
+          const float2 X = __ffma2_rn(xr, xscale, __fmul2_rn(du, gp));  // + correction's difference
           const float2 X2 = __fmul2_rn(X, X);
-          const float2 sx = __ffma2_rn(X, __fmul2_rn(X2, __ffma2_rn(X2, s5, s3)), X);  // sin X
-          const float2 cx = __fmul2_rn(X2, __ffma2_rn(X2, c4, nhalf2));               // cos X - 1
-          const float2 cr = __fadd2_rn(cx, l0);          // e^{l0} e^{iX} - 1, real part
-          const float2 ci = __ffma2_rn(sx, l0, sx);      //                   imaginary part
-          const int ka = int(ea >> 26), kb = int(eb >> 26);
+          const float2 sx = __ffma2_rn(X, __fmul2_rn(X2, s3), X);  // sin X
+          const float2 cr = __ffma2_rn(X2, nhalf2, l0);            // e^{l0} e^{iX} - 1, real
+          const float2 ci = __ffma2_rn(sx, l0, sx);                //                    imaginary
+          const int ka = int(ea >> 24), kb = int(eb >> 24);
           const float2 tr = make_float2(s_tr[ka], s_tr[kb]), ti = make_float2(s_ti[ka], s_ti[kb]);
           const float2 t0 = __ffma2_rn(ti, ci, make_float2(-tr.x, -tr.y));  // ti ci - tr
           vr = __ffma2_rn(tr, cr, make_float2(-t0.x, -t0.y));               // tr (1 + cr) - ti ci
@@ -380,10 +388,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           const float2 dmu = __ffma2_rn(fx, cmid_a, cmid_b);  // u(x + L/2) - um
           const float2 gpm = __ffma2_rn(gpp, dmu, gp);        // G h'(u(x + L/2))
           const float2 upm = __ffma2_rn(fx, c2, cL);          // u'(x + L/2) = 2c (x + L/2)
-          const float2 dl = __ffma2_rn(gpp, __fmul2_rn(upm, upm), __ffma2_rn(gpm, c2, dq2));
-          const float2 dl2 = __fmul2_rn(dl, dl);
-          sr = __ffma2_rn(dl2, nhalf2, lc2);                  // l2 - delta^2/2
-          si = __ffma2_rn(dl, __fmul2_rn(dl2, s3), dl);       // delta - delta^3/6
+          // si = delta - delta^3/6 = dq - dq^3/6 + delta_c (delta_c: the correction's part)
+          si = __ffma2_rn(gpp, __fmul2_rn(upm, upm), __ffma2_rn(gpm, c2, dq3));
+          // sr = l2 - delta^2/2 = -c - dq^2/2 - dq delta_c
+          sr = __ffma2_rn(si, ndq, sr0);
         }
 
 #pragma unroll
@@ -555,15 +563,27 @@ struct LaunchArgs {
   size_t stride;
 };
 
+int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled, tuning)
+  static const int u = [] {
+    const char* e = std::getenv("WCGH_DIRECT_RU");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return u;
+}
+
 template <int NC, int AMP>
 void launch_rec(const LaunchArgs& a) {
   constexpr int MINB = 2;
-  if (a.cplx)
-    k_direct_rec<NC, AMP, MINB, true><<<a.grid, kThreads, 0, a.s>>>(
-        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
-  else
-    k_direct_rec<NC, AMP, MINB, false><<<a.grid, kThreads, 0, a.s>>>(
-        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride);
+#define WCGH_REC(CPLX_, RU_)                                                              \
+  k_direct_rec<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(                 \
+      a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride)
+  const bool u2 = rec_unroll() == 2;
+  if (a.cplx) {
+    if (u2) WCGH_REC(true, 2); else WCGH_REC(true, 1);
+  } else {
+    if (u2) WCGH_REC(false, 2); else WCGH_REC(false, 1);
+  }
+#undef WCGH_REC
 }
 
 template <int NC>
@@ -665,7 +685,17 @@ DirectLayer make_direct_layer(const wcgh_layer& L) {
   // second difference of the quadratic phase between adjacent pixels: 2 alpha
   // cycles, centred (the recurrence rotates by it each step)
   const double f2 = 2.0 * alpha - std::nearbyint(2.0 * alpha);
-  d.dq = float(two_pi * f2);
+  const double dq = two_pi * f2;
+  d.dq = float(dq);
+  d.dq3 = float(dq - dq * dq * dq / 6.0);
+  d.sr0 = float(dq * (dq - dq * dq * dq / 6.0) - 0.5 * dq * dq - p * p / (z * z));
+  // run B (16 pixels right of run A): t_B - t_A = alpha (32 dx + 256)
+  //   = 16 D_A + alpha * 240,  D_B - D_A = 32 alpha  (0.32 fixed point, mod 1)
+  const auto fix32 = [](double v) {
+    return uint32_t(uint64_t(std::llround(std::ldexp(v - std::floor(v), 32))) & 0xffffffffu);
+  };
+  d.t_ab = fix32(240.0 * fa);
+  d.d_ab = fix32(32.0 * fa);
   d.wavelength = lam;
   d.pitch = p;
   d.z = z;

@@ -182,7 +182,8 @@ struct DirectLayer {
   // quadratic phase's second difference between adjacent pixels, 2 alpha
   // cycles, centred and in radians.
   float dcorr[kMaxCorr], ddcorr[kMaxCorr];
-  float dq;
+  float dq, dq3, sr0;     // dq, dq - dq^3/6, -c + dq (dq - dq^3/6) - dq^2/2
+  uint32_t t_ab, d_ab;    // frac(240 alpha), frac(32 alpha): run B from run A (L = 16)
   double wavelength, pitch, z, k;  // fp64 phase mode
 };
 
