@@ -430,6 +430,258 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Chirp-factored recurrence (default fixed-point form, P = 32). The
+// quadratic phase splits exactly along a run:
+//   2 pi alpha (dx + i)^2 = 2 pi alpha dx^2 + 2 pi (2 alpha dx) i + 2 pi alpha i^2,
+// and Q_i = e^{2 pi i alpha i^2} is the same for every point and every run,
+// so it is factored out of the point sum: the kernel accumulates
+// Z_i = sum_j z_i^(j) with z_i = w_i / Q_i and multiplies by Q_i once at the
+// end (a chunk that crosses into another layer re-frames Z by Q/Q' there).
+// z's step ratio v_i then varies only through the small non-paraxial
+// correction and the amplitude (second difference sigma_c ~ 1e-5 rad at the
+// config-4 corner), so v_i = v_0 (1 + sigma_c)^i = v_0 + i g to O(i^2
+// sigma_c^2) (< 1e-8): a pixel costs one complex multiply, one complex
+// add and one complex fma (8 lane operations) instead of two complex
+// multiplies. Seeds as in k_direct_rec (exact fixed-point w_0 with 2 MUFU;
+// v_0 from the exact fixed-point frac(2 alpha dx) through the 256-entry table
+// and short polynomials), g = v_0 (l2 + i dc_mid).
+// Multiplies the accumulators by Q_i^(from) / Q_i^(to) (to < 0: by Q_i^(from)).
+// CTA-uniform (layer spans depend on the chunk only): 16 threads evaluate the
+// factors in fp64 into shared memory, every thread applies them.
+__device__ __forceinline__ void rotate_chirp(float2 (&hr)[16], float2 (&hi)[16], int from, int to,
+                                             float2* s_q) {
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    const uint32_t ii = threadIdx.x * threadIdx.x;
+    const DirectLayer& F = c_layers[from];
+    uint32_t t = ii * F.a_hi + __umulhi(ii, F.a_lo);
+    if (to >= 0) {
+      const DirectLayer& T = c_layers[to];
+      t -= ii * T.a_hi + __umulhi(ii, T.a_lo);
+    }
+    double sn, cs;
+    sincospi(double(int32_t(t)) * (1.0 / 2147483648.0), &sn, &cs);
+    s_q[threadIdx.x] = make_float2(float(cs), float(sn));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 q = s_q[i];
+    const float2 qc = make_float2(q.x, q.x), qs = make_float2(q.y, q.y);
+    const float2 t = __fmul2_rn(hi[i], qs);
+    const float2 nr = __ffma2_rn(hr[i], qc, make_float2(-t.x, -t.y));
+    hi[i] = __ffma2_rn(hi[i], qc, __fmul2_rn(hr[i], qs));
+    hr[i] = nr;
+  }
+}
+
+template <int NC, int AMP, int MINB, bool CPLX, int RU>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_direct_chirp(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
+                 int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
+                 int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
+  constexpr int L = 16;  // run length; 2 runs per thread
+  __shared__ int4 sp[kBatch];
+  __shared__ float s_tr[256], s_ti[256];
+  __shared__ float2 s_q[16];
+  {
+    double sn, cs;
+    sincospi(double(threadIdx.x) / 128.0, &sn, &cs);
+    s_tr[threadIdx.x] = float(cs);
+    s_ti[threadIdx.x] = float(sn);
+  }
+  static_assert(kThreads == 256, "one table entry per thread");
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int tx = blockIdx.x % tiles_x;
+  const int ty = blockIdx.x / tiles_x;
+  const int row = ty * 8 + warp;
+  const int y = row0 + row;
+  const int x0 = tx * 1024 + 32 * lane;
+  const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
+  const long long p1 = min(p0 + kChunk, n_points);
+
+  // hr[i] = (re of pixel x0 + i, re of pixel x0 + L + i); hi likewise
+  float2 hr[L], hi[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) hr[i] = hi[i] = make_float2(0.0f, 0.0f);
+
+  int cur = -1;  // layer whose chirp frame the accumulators are in
+  for (int l = 0; l < n_layers; ++l) {
+    long long s0, s1;
+    layer_span(layer_begin, l, p0, p1, s0, s1);
+    if (s0 >= s1) continue;
+    if (cur >= 0) rotate_chirp(hr, hi, cur, l, s_q);  // a chunk spanning two layers (rare)
+    cur = l;
+    const DirectLayer& Ly = c_layers[l];
+    const uint32_t a_hi = Ly.a_hi, a_lo = Ly.a_lo, phi0 = Ly.phi0;
+    const uint32_t t_ab = Ly.t_abq, d_ab = Ly.d_ab;
+    const float c = Ly.c, inv_z = Ly.inv_z;
+    float2 corr[NC], dcorr[NC], ddcorr[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      corr[k] = make_float2(Ly.corr[k], Ly.corr[k]);
+      dcorr[k] = make_float2(Ly.dcorr[k], Ly.dcorr[k]);
+      ddcorr[k] = make_float2(Ly.ddcorr[k], Ly.ddcorr[k]);
+    }
+    const float am1 = Ly.amp[0], am2 = Ly.amp[1], am3 = Ly.amp[2];
+    const float2 two_pi2 = make_float2(kTwoPi, kTwoPi);
+    const float2 neg3pi2 = make_float2(kNegThreePi, kNegThreePi);
+    const float2 c2 = make_float2(2.0f * c, 2.0f * c), cc = make_float2(c, c);
+    const float2 half2 = make_float2(0.5f, 0.5f), nhalf2 = make_float2(-0.5f, -0.5f);
+    const float2 cmid_a = make_float2(c * float(L - 1), c * float(L - 1));
+    const float2 cmid_b = make_float2(c * (float(L * L) * 0.25f - 0.5f), c * (float(L * L) * 0.25f - 0.5f));
+    const float2 cL = make_float2(c * float(L), c * float(L));
+    const float2 nc2 = make_float2(-c, -c);
+    const float2 xscale = make_float2(kTwoPi / 2147483648.0f, kTwoPi / 2147483648.0f);  // 2pi / 2^31
+    const float2 s3 = make_float2(-1.0f / 6.0f, -1.0f / 6.0f);
+
+    for (long long b = s0; b < s1; b += kBatch) {
+      const int nb = int(min((long long)kBatch, s1 - b));
+      __syncthreads();
+      for (int i = threadIdx.x; i < nb; i += kThreads) {
+        WCGH_DCHECK(b + i < n_points && b + i >= 0);
+        int4 r = pts[b + i];
+        // real amplitudes: stage a0 = A/z and a0 * am1 once per CTA instead
+        // of once per thread (complex records keep their phase in .w)
+        const float a0 = __int_as_float(r.z) * inv_z;
+        r.z = __float_as_int(a0);
+        if (!CPLX) r.w = __float_as_int(a0 * am1);
+        sp[i] = r;
+      }
+      __syncthreads();
+
+#pragma unroll RU
+      for (int j = 0; j < nb; ++j) {
+        const int4 q = sp[j];
+        const int dxa = x0 - q.x;
+        const int dy = y - q.y;
+        const uint32_t ph0 = CPLX ? phi0 + uint32_t(q.w) : phi0;
+        const int sa = dxa * dxa + dy * dy;
+        const int sb = sa + (2 * L) * dxa + L * L;
+        const uint32_t ta = uint32_t(sa) * a_hi + __umulhi(uint32_t(sa), a_lo) + ph0;
+        // linear part of the quadratic phase's first difference: frac(2 alpha dx), exact
+        const int ma = 2 * dxa;
+        const uint32_t da = uint32_t(ma) * a_hi + uint32_t(((long long)ma * (long long)a_lo) >> 32);
+        const uint32_t tb = ta + (da << 4) + t_ab;  // L = 16: t_B - t_A = 16 * 2 alpha dx + 256 alpha
+        const uint32_t db = da + d_ab;
+
+        const float2 fx = make_float2(i2f_small(dxa), i2f_small(dxa + L));
+        const float2 U = __fmul2_rn(make_float2(__int2float_rn(sa), __int2float_rn(sb)), cc);
+
+        // ---- seed w_0 (the fixed kernel's per-pixel evaluation)
+        float2 wr, wi;
+        {
+          const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
+                                         __int_as_float((tb >> 9) | 0x3f800000u));
+          const float2 u2 = __fmul2_rn(U, U);
+          float2 pc = corr[NC - 1];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
+          const float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
+          const float a0 = __int_as_float(q.z);
+          const float2 A0 = make_float2(a0, a0);
+          float2 am;
+          if constexpr (AMP == 3) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2),
+                         A3 = make_float2(a0 * am3, a0 * am3);
+            am = __ffma2_rn(__ffma2_rn(__ffma2_rn(A3, U, A2), U, A1), U, A0);
+          } else if constexpr (AMP == 2) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2);
+            am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
+          } else if constexpr (AMP == 1) {
+            const float a1 = CPLX ? a0 * am1 : __int_as_float(q.w);
+            am = __ffma2_rn(make_float2(a1, a1), U, A0);
+          } else {
+            am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
+          }
+          float2 sn, cs;
+          __sincosf(ph.x, &sn.x, &cs.x);
+          __sincosf(ph.y, &sn.y, &cs.y);
+          wr = __fmul2_rn(am, cs);
+          wi = __fmul2_rn(am, sn);
+        }
+
+        // ---- seed v_0 and its per-step increment g
+        float2 vr, vi, gr, gi;
+        {
+          const float2 du = __ffma2_rn(fx, c2, cc);      // u(x+1) - u(x) = c (2x + 1)
+          const float2 um = __ffma2_rn(du, half2, U);    // u at x + 1/2
+          float2 gq = dcorr[NC - 1], gpp = ddcorr[NC - 1];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) {
+            gq = __ffma2_rn(gq, um, dcorr[k]);
+            gpp = __ffma2_rn(gpp, um, ddcorr[k]);
+          }
+          const float2 gp = __fmul2_rn(gq, um);          // G h'(um), radians per unit u
+          const float2 l0 = __fmul2_rn(du, nhalf2);      // ln a(x+1) - ln a(x) = -du/2 (1 - O(u))
+          // quadratic part: table entry k = round(D / 2^24) and the remainder
+          const uint32_t ea = da + (1u << 23), eb = db + (1u << 23);
+          const float2 xr = make_float2(
+              __int_as_float(0x4b000000u | ((ea & 0xffffffu) >> 1)) - 12582912.0f,
+              __int_as_float(0x4b000000u | ((eb & 0xffffffu) >> 1)) - 12582912.0f);
+          const float2 X = __ffma2_rn(xr, xscale, __fmul2_rn(du, gp));  // + correction's difference
+          const float2 X2 = __fmul2_rn(X, X);
+          const float2 sx = __ffma2_rn(X, __fmul2_rn(X2, s3), X);  // sin X
+          const float2 cr = __ffma2_rn(X2, nhalf2, l0);            // e^{l0} e^{iX} - 1, real
+          const float2 ci = __ffma2_rn(sx, l0, sx);                //                    imaginary
+          const int ka = int(ea >> 24), kb = int(eb >> 24);
+          const float2 tr = make_float2(s_tr[ka], s_tr[kb]), ti = make_float2(s_ti[ka], s_ti[kb]);
+          const float2 t0 = __ffma2_rn(ti, ci, make_float2(-tr.x, -tr.y));  // ti ci - tr
+          vr = __ffma2_rn(tr, cr, make_float2(-t0.x, -t0.y));               // tr (1 + cr) - ti ci
+          vi = __ffma2_rn(ti, cr, __ffma2_rn(tr, ci, ti));                  // ti (1 + cr) + tr ci
+          // the correction's second difference at the run's middle x + L/2
+          const float2 dmu = __ffma2_rn(fx, cmid_a, cmid_b);  // u(x + L/2) - um
+          const float2 gpm = __ffma2_rn(gpp, dmu, gp);        // G h'(u(x + L/2))
+          const float2 upm = __ffma2_rn(fx, c2, cL);          // u'(x + L/2) = 2c (x + L/2)
+          const float2 dc = __ffma2_rn(gpp, __fmul2_rn(upm, upm), __fmul2_rn(gpm, c2));
+          // g = v_0 (l2 + i dc), l2 = -c: v_i = v_0 (1 + sigma_c)^i = v_0 + i g + O(i^2 dc^2)
+          const float2 tg = __fmul2_rn(vi, dc);
+          gr = __ffma2_rn(vr, nc2, make_float2(-tg.x, -tg.y));
+          gi = __ffma2_rn(vi, nc2, __fmul2_rn(vr, dc));
+        }
+
+        // z_i (w_i without the common chirp Q_i): z_{i+1} = z_i v_i, v_i = v_0 + i g
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          hr[i] = __fadd2_rn(hr[i], wr);
+          hi[i] = __fadd2_rn(hi[i], wi);
+          if (i < L - 1) {
+            float2 ur = vr, ui = vi;
+            if (i > 0) {
+              const float2 fi = make_float2(float(i), float(i));
+              ur = __ffma2_rn(gr, fi, vr);
+              ui = __ffma2_rn(gi, fi, vi);
+            }
+            const float2 t1 = __fmul2_rn(wi, ui), t2 = __fmul2_rn(wi, ur);
+            const float2 nwr = __ffma2_rn(wr, ur, make_float2(-t1.x, -t1.y));
+            wi = __ffma2_rn(wr, ui, t2);
+            wr = nwr;
+          }
+        }
+      }
+    }
+  }
+
+  if (cur >= 0) rotate_chirp(hr, hi, cur, -1, s_q);  // H_i = Z_i Q_i
+  if (row < rows) {
+    float2* dst = out + blockIdx.y * out_chunk_stride + size_t(row) * nh;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int p = 2 * m, x = x0 + p;
+      const float4 r = p < L ? make_float4(hr[p].x, hi[p].x, hr[p + 1].x, hi[p + 1].x)
+                             : make_float4(hr[p - L].y, hi[p - L].y, hr[p - L + 1].y, hi[p - L + 1].y);
+      WCGH_DCHECK(x >= nh || size_t(blockIdx.y) * out_chunk_stride + size_t(row) * nh + x <
+                                 size_t(gridDim.y) * out_chunk_stride);
+      if (x + 1 < nh)
+        *reinterpret_cast<float4*>(dst + x) = r;
+      else if (x < nh)
+        dst[x] = make_float2(r.x, r.y);
+    }
+  }
+}
+
+
 // Double-phase option: r and k*r in fp64, reduced to [-pi, pi] in fp64, then
 // fp32 sin/cos. Accuracy mode (FP64-pipe bound).
 template <int P>
@@ -572,11 +824,15 @@ int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled,
 }
 
 template <int NC, int AMP>
-void launch_rec(const LaunchArgs& a) {
+void launch_rec(const LaunchArgs& a, bool chirp) {
   constexpr int MINB = 2;
 #define WCGH_REC(CPLX_, RU_)                                                              \
-  k_direct_rec<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(                 \
-      a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride)
+  if (chirp)                                                                              \
+    k_direct_chirp<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(             \
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride); \
+  else                                                                                    \
+    k_direct_rec<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(               \
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride)
   const bool u2 = rec_unroll() == 2;
   if (a.cplx) {
     if (u2) WCGH_REC(true, 2); else WCGH_REC(true, 1);
@@ -588,14 +844,15 @@ void launch_rec(const LaunchArgs& a) {
 
 template <int NC>
 void launch_rec_amp(const DirectPlan& plan, const LaunchArgs& a) {
+  const bool chirp = plan.rec == 2;
   if (plan.amp_degree == 1)
-    launch_rec<NC, 1>(a);
+    launch_rec<NC, 1>(a, chirp);
   else if (plan.amp_degree == 2)
-    launch_rec<NC, 2>(a);
+    launch_rec<NC, 2>(a, chirp);
   else if (plan.amp_degree == 3)
-    launch_rec<NC, 3>(a);
+    launch_rec<NC, 3>(a, chirp);
   else
-    launch_rec<NC, 0>(a);
+    launch_rec<NC, 0>(a, chirp);
 }
 
 void launch_rec_nc(const DirectPlan& plan, const LaunchArgs& a) {
@@ -695,6 +952,7 @@ DirectLayer make_direct_layer(const wcgh_layer& L) {
     return uint32_t(uint64_t(std::llround(std::ldexp(v - std::floor(v), 32))) & 0xffffffffu);
   };
   d.t_ab = fix32(240.0 * fa);
+  d.t_abq = fix32(256.0 * fa);  // chirp form: t_B - t_A = 16 frac(2 alpha dx) + 256 alpha
   d.d_ab = fix32(32.0 * fa);
   d.wavelength = lam;
   d.pitch = p;
@@ -782,11 +1040,12 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     // evaluation (k_direct_fixed) for comparisons.
     static const int rec_env = [] {
       const char* e = std::getenv("WCGH_DIRECT_REC");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
-    bool rec = rec_env != 0 && pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02;
-    for (int l = 0; l < n_layers; ++l) rec = rec && std::fabs(h_layers[l].dq) <= 0.03f;
-    plan.rec = rec;
+    const bool ok = pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02;
+    bool small_dq = true;  // k_direct_rec expands the quadratic second difference
+    for (int l = 0; l < n_layers; ++l) small_dq = small_dq && std::fabs(h_layers[l].dq) <= 0.03f;
+    plan.rec = !ok || rec_env == 0 ? 0 : (rec_env == 1 ? (small_dq ? 1 : 0) : 2);
   }
   WCGH_CUDA(cudaMemcpyToSymbolAsync(c_layers, h_layers, sizeof(DirectLayer) * n_layers, 0,
                                     cudaMemcpyHostToDevice, stream));

@@ -184,6 +184,7 @@ struct DirectLayer {
   float dcorr[kMaxCorr], ddcorr[kMaxCorr];
   float dq, dq3, sr0;     // dq, dq - dq^3/6, -c + dq (dq - dq^3/6) - dq^2/2
   uint32_t t_ab, d_ab;    // frac(240 alpha), frac(32 alpha): run B from run A (L = 16)
+  uint32_t t_abq;         // frac(256 alpha): the same for the chirp-factored form
   double wavelength, pitch, z, k;  // fp64 phase mode
 };
 
@@ -191,7 +192,8 @@ struct DirectPlan {
   int n_corr;      // phase-series terms used (2, 3, 5 or 8)
   int amp_degree;  // (1+u)^(-1/2): polynomial degree 1, 2 or 3, or 0 = MUFU.RSQ
   double u_max;
-  bool rec;        // angle-addition recurrence along 16-pixel runs (k_direct_rec)
+  int rec;         // 0 per-pixel (k_direct_fixed); angle-addition recurrence along
+                   // 16-pixel runs: 1 k_direct_rec, 2 chirp-factored k_direct_chirp
 };
 
 // CUDA-event pairs around each launch of a kernel family (for per-kernel
