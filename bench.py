@@ -43,6 +43,11 @@ UNIT = "updates/s"
 SM_COUNT = 148
 MUFU_PER_CLK_SM = 16.0
 CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
+# K3 as built (k_direct_chirp, point loop unrolled by 2): per point and thread
+# (32 updates) 158 packed fp32x2 FMA-pipe instructions (config 4, NC = 3; 155 at
+# NC = 2) + ~12 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
+K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
+K3_LANE_OPS_PER_UPDATE = 10.0
 E2E_SECONDS = 60.0          # e2e / alt-method step budget at large configs
 ALT_SECONDS = 10.0
 
@@ -490,13 +495,15 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
     rank_updates = float(points) * rows * c.plane_size
     achieved = rank_updates / (k_ms * 1e-3) if k_ms > 0 else None
     if job.spec.method == "direct":
-        per_clk, kernel = MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE, "k_direct_fixed (K3)"
+        per_clk, kernel = MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE, K3_KERNEL
         basis = (f"canonical SFU roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz (MEASURED_PEAKS "
-                 "sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)); the kernel "
-                 "issues 2 MUFU + packed-fp32x2/ALU issue slots per update, so its own "
-                 "bound is 2 MUFU per update (frac_of_2mufu_bound); not an HBM or "
-                 "tensor-core kernel")
-        bound, key = "sfu", "k_direct_fixed"
+                 "sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)). K3 "
+                 "evaluates exp(ikr)/r by angle addition along 16-pixel runs (2 MUFU per run "
+                 "seed, 4 per 32 updates), so it is bound by the FP32 pipe instead: "
+                 "frac_of_fp32_bound = achieved / (148 x f x 128 lane-ops/clk/SM / "
+                 f"{K3_LANE_OPS_PER_UPDATE} lane-ops per update, counted from the SASS in "
+                 "profiles/sass/k3_direct_chirp_NC3_AMP1_RU2.sass); not an HBM or tensor-core kernel")
+        bound, key = "sfu", "k_direct_chirp"
         dram = int(points * 16 + rows * c.plane_size * 8)
     elif job.spec.method == "lut":
         per_clk, kernel = 128.0 / 2.0, "k_lut_stage (K4), 4 stage launches"
@@ -537,7 +544,10 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
                                 "capture; dominated by the fixed-order fp32 partial-sum planes "
                                 "(compute-bound kernel, < 1% DRAM utilisation)")
     if bound == "sfu" and achieved:
-        roof["frac_of_2mufu_bound"] = achieved / (SM_COUNT * f_max * MUFU_PER_CLK_SM / 2.0)
+        fp32_peak = SM_COUNT * f_max * 128.0 / K3_LANE_OPS_PER_UPDATE
+        roof["fp32_bound"] = fp32_peak
+        roof["frac_of_fp32_bound"] = achieved / fp32_peak
+        roof["fp32_lane_ops_per_update"] = K3_LANE_OPS_PER_UPDATE
     return roof
 
 

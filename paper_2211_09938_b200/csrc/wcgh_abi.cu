@@ -333,7 +333,9 @@ int wcgh_synth_points(wcgh_ctx* ctx, const wcgh_point* points, int64_t n_points,
       prev = p.layer;
       lb[size_t(p.layer) + 1]++;
       max_dx = std::max({max_dx, std::fabs(double(p.x)), std::fabs(double(nh - 1 - p.x))});
-      max_dy = std::max({max_dy, std::fabs(double(p.y - row0)), std::fabs(double(row0 + rows - 1 - p.y))});
+      // the series plan covers the whole plane, not just the band, so any row
+      // band of it is bitwise the same rows of the full plane (fixed chunks)
+      max_dy = std::max({max_dy, std::fabs(double(p.y)), std::fabs(double(nh - 1 - p.y))});
     }
     require(max_dx < 32768 && max_dy < 32768, "synth_points: offsets beyond 32767 pixels");
     for (int l = 0; l < n_layers; ++l) lb[size_t(l) + 1] += lb[size_t(l)];

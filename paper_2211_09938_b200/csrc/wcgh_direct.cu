@@ -816,11 +816,8 @@ struct LaunchArgs {
 };
 
 int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled, tuning)
-  static const int u = [] {
-    const char* e = std::getenv("WCGH_DIRECT_RU");
-    return e && std::atoi(e) == 1 ? 1 : 2;
-  }();
-  return u;
+  const char* e = std::getenv("WCGH_DIRECT_RU");
+  return e && std::atoi(e) == 1 ? 1 : 2;
 }
 
 template <int NC, int AMP>
@@ -1036,12 +1033,11 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     // the recurrence form: 32 consecutive pixels per thread (P = 32, float4
     // stores need an even width), small per-pixel rotation of the quadratic
     // phase and a small u (the series of sigma and of the log-amplitude
-    // differences, see k_direct_rec). WCGH_DIRECT_REC=0 forces the per-pixel
-    // evaluation (k_direct_fixed) for comparisons.
-    static const int rec_env = [] {
-      const char* e = std::getenv("WCGH_DIRECT_REC");
-      return e ? std::atoi(e) : 2;
-    }();
+    // differences, see k_direct_rec). WCGH_DIRECT_REC selects the form for
+    // comparisons: 0 per-pixel (k_direct_fixed), 1 k_direct_rec, 2 (default)
+    // the chirp-factored k_direct_chirp.
+    const char* rec_e = std::getenv("WCGH_DIRECT_REC");  // read per call (tests switch it)
+    const int rec_env = rec_e ? std::atoi(rec_e) : 2;
     const bool ok = pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02;
     bool small_dq = true;  // k_direct_rec expands the quadratic second difference
     for (int l = 0; l < n_layers; ++l) small_dq = small_dq && std::fabs(h_layers[l].dq) <= 0.03f;

@@ -1,0 +1,88 @@
+"""The three evaluation forms of K3 (direct point-source accumulation,
+tests/support/oracles.cpp:12-36) against the fp64 direct Eq.(1) oracle and
+against each other, through the C ABI (wcgh_synth_points):
+
+  * WCGH_DIRECT_REC=0 — k_direct_fixed: exp(ikr)/r per (point, pixel) from the
+    fixed-point phase (2 MUFU per update);
+  * WCGH_DIRECT_REC=1 — k_direct_rec: angle addition along 16-pixel runs with
+    the full second difference;
+  * WCGH_DIRECT_REC=2 (default) — k_direct_chirp: the same with the common
+    chirp e^{2 pi i alpha i^2} factored out of the point sum.
+
+The plane width (1500) is not a multiple of the 1024-pixel tile, the 3000
+points span three 1024-point chunks, and they belong to two depth layers
+with the layer boundary inside the second chunk, so the chirp form's
+re-framing of its accumulators between layers (rotate_chirp) runs."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2211_09938_b200 import _lib, stages
+
+pytestmark = pytest.mark.gpu
+
+WL = 532e-9
+LAYERS = [(WL, 8e-6, 0.2), (WL, 8e-6, 0.25)]
+NH = 1500
+
+
+def _points():
+    rng = np.random.default_rng(2024)
+    n0, n1 = 1700, 1300
+    pts = np.zeros(n0 + n1, _lib.POINT_DTYPE)
+    lo, hi = NH // 2 - 400, NH // 2 + 400
+    for sl, lay in ((slice(0, n0), 0), (slice(n0, n0 + n1), 1)):
+        k = sl.stop - sl.start
+        pts["x"][sl] = rng.integers(lo, hi, k)
+        pts["y"][sl] = rng.integers(lo, hi, k)
+        pts["a"][sl] = rng.integers(1, 256, k).astype(np.float32)
+        pts["layer"][sl] = lay
+    return pts
+
+
+def _oracle_rows(pts, rows):
+    py, px = np.meshgrid(np.asarray(rows), np.arange(NH), indexing="ij")
+    ref = O.direct_pixels(pts["x"], pts["y"], pts["a"], pts["layer"], LAYERS, px.ravel(),
+                          py.ravel())
+    return ref.reshape(len(rows), NH)
+
+
+ROWS = (0, 1, 377, 750, 1499)
+
+
+@pytest.fixture(scope="module")
+def reference():
+    pts = _points()
+    return pts, _oracle_rows(pts, ROWS)
+
+
+@pytest.mark.parametrize("form", ["0", "1", "2"])
+def test_direct_forms_vs_fp64_oracle(ctx, monkeypatch, reference, form):
+    pts, ref = reference
+    monkeypatch.setenv("WCGH_DIRECT_REC", form)
+    got = np.stack([stages.synth_points(pts, LAYERS, NH, row0=r, rows=1)[0] for r in ROWS])
+    err = O.rel_l2(got, ref)
+    # the recurrence forms are as accurate as the per-pixel form (their
+    # seeds are exact, the runs add ~1e-6 rad); all far inside the 1e-4 bar
+    assert err <= 1e-5, (form, err)
+
+
+def test_direct_forms_agree_on_a_band(ctx, monkeypatch):
+    """A 64-row band through all three forms (and the point loop not
+    unrolled): the recurrence forms agree with the per-pixel form to the
+    fp32 level, and each band equals the same rows of the full plane
+    bitwise (fixed-order chunks)."""
+    pts = _points()
+    out = {}
+    for form, ru in (("0", "2"), ("1", "2"), ("2", "2"), ("2", "1")):
+        monkeypatch.setenv("WCGH_DIRECT_REC", form)
+        monkeypatch.setenv("WCGH_DIRECT_RU", ru)
+        out[form, ru] = stages.synth_points(pts, LAYERS, NH, row0=700, rows=64)
+    base = out["0", "2"]
+    for k, v in out.items():
+        assert O.rel_l2(v, base) <= 1e-5, k
+    assert np.array_equal(out["2", "1"], out["2", "2"]) or O.rel_l2(out["2", "1"], out["2", "2"]) <= 1e-6
+    monkeypatch.setenv("WCGH_DIRECT_REC", "2")
+    monkeypatch.delenv("WCGH_DIRECT_RU")
+    full = stages.synth_points(pts, LAYERS, NH)
+    assert np.array_equal(full[700:764], out["2", "2"])

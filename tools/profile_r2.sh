@@ -18,7 +18,7 @@ fi
 if [ -z "${SKIP_K3:-}" ]; then
 timeout 900 $B4 > "$OUT/plain4b_$TAG.log" 2>&1 && \
   timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_direct_fixed" -s 2 -c 1 -o "$OUT/prof_k3_cfg4_$TAG" $B4 > "$OUT/ncu_k3_$TAG.log" 2>&1; echo "ncu_k3=$?"
+    -k "regex:k_direct_chirp" -s 2 -c 1 -o "$OUT/prof_k3_cfg4_$TAG" $B4 > "$OUT/ncu_k3_$TAG.log" 2>&1; echo "ncu_k3=$?"
 fi
 if [ -z "${SKIP_K4:-}" ]; then
 timeout 300 $B2 > "$OUT/plain2_$TAG.log" 2>&1 && \

@@ -18,7 +18,7 @@ timeout 300 $B1 > "$OUT/plain1_$TAG.log" 2>&1 && \
     --log-file "$OUT/launches_cfg1_$TAG.csv" $B1 > "$OUT/ncu1_$TAG.log" 2>&1; echo "ncu_launch=$?"
 timeout 300 $B1 > "$OUT/plain2_$TAG.log" 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_analysis|k_direct_fixed" -s 2 -c 2 -o "$OUT/prof_k3_$TAG" $B1 > "$OUT/ncu2_$TAG.log" 2>&1; echo "ncu_k3=$?"
+    -k "regex:k_analysis|k_direct_chirp" -s 2 -c 2 -o "$OUT/prof_k3_$TAG" $B1 > "$OUT/ncu2_$TAG.log" 2>&1; echo "ncu_k3=$?"
 timeout 300 $B2 > "$OUT/plain3_$TAG.log" 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
     -k "regex:k_lut_stage" -s 4 -c 4 -o "$OUT/prof_k4_$TAG" $B2 > "$OUT/ncu3_$TAG.log" 2>&1; echo "ncu_k4=$?"
