@@ -278,9 +278,28 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
       float wt[S - 1];
 #pragma unroll
       for (int k = 0; k < S - 1; ++k) wt[k] = ws[full + k];
+      // ptxas if-converts a straight-line remainder block (each step guarded
+      // by uu < rem), so a block costs all its step slots whatever rem is:
+      // three blocks of 1/3, 2/3 and all of the S - 1 slots keep the
+      // predicated-off slots under a third of the block (config 2 K4 29.73 ->
+      // 29.39 ms; one block per remainder length via a jump table measured
+      // the same, 29.39 ms, at twice the code).
+      constexpr int T1 = (S - 1) / 3, T2 = 2 * (S - 1) / 3;
+      if (rem <= T1) {
 #pragma unroll
-      for (int uu = 0; uu < S - 1; ++uu) {
-        if (uu < rem) WCGH_LUT_STEP_W(uu, wt[uu])
+        for (int uu = 0; uu < T1; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, wt[uu])
+        }
+      } else if (rem <= T2) {
+#pragma unroll
+        for (int uu = 0; uu < T2; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, wt[uu])
+        }
+      } else {
+#pragma unroll
+        for (int uu = 0; uu < S - 1; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, wt[uu])
+        }
       }
     }
 #undef WCGH_LUT_STEP_W
