@@ -1038,7 +1038,22 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     // the chirp-factored k_direct_chirp.
     const char* rec_e = std::getenv("WCGH_DIRECT_REC");  // read per call (tests switch it)
     const int rec_env = rec_e ? std::atoi(rec_e) : 2;
-    const bool ok = pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02;
+    // The runs neglect the correction's third difference (phase error <=
+    // L^3/12 * phi''' at the run end, phi''' ~ 3 G c^2 |dx|) and the chirp
+    // form linearises the multiplier (error ~ C(L-1, 2) dc^2, dc ~ G c^2
+    // (3 dx^2 + dy^2) / 2): both must stay far below the 1e-4 bar at the
+    // farthest (pixel, point) pair, else the per-pixel form runs (configs
+    // 1-4: 1.2e-6 .. 9.5e-6 rad and < 1e-8; a 20 um pitch at z = 0.2 m would
+    // be 2e-4 rad).
+    bool curv_ok = true;
+    for (int l = 0; l < n_layers; ++l) {
+      const double G = 2.0 * 3.141592653589793 * layers[l].z / layers[l].wavelength;
+      const double cl = layers[l].pitch * layers[l].pitch / (layers[l].z * layers[l].z);
+      const double e3 = (16.0 * 16.0 * 16.0 / 12.0) * 3.0 * G * cl * cl * max_dx;
+      const double dcm = G * cl * cl * (3.0 * max_dx * max_dx + max_dy * max_dy) / 2.0;
+      curv_ok = curv_ok && e3 <= 2e-5 && 105.0 * dcm * dcm <= 1e-6;
+    }
+    const bool ok = pixels_per_thread(nh) == 32 && nh % 2 == 0 && plan.u_max <= 0.02 && curv_ok;
     bool small_dq = true;  // k_direct_rec expands the quadratic second difference
     for (int l = 0; l < n_layers; ++l) small_dq = small_dq && std::fabs(h_layers[l].dq) <= 0.03f;
     plan.rec = !ok || rec_env == 0 ? 0 : (rec_env == 1 ? (small_dq ? 1 : 0) : 2);

@@ -58,6 +58,7 @@ def reference():
 
 @pytest.mark.parametrize("form", ["0", "1", "2"])
 def test_direct_forms_vs_fp64_oracle(ctx, monkeypatch, reference, form):
+    """Two depth layers on a 1500-wide plane (8 um pitch, z 0.20 / 0.25 m)."""
     pts, ref = reference
     monkeypatch.setenv("WCGH_DIRECT_REC", form)
     got = np.stack([stages.synth_points(pts, LAYERS, NH, row0=r, rows=1)[0] for r in ROWS])
@@ -86,3 +87,45 @@ def test_direct_forms_agree_on_a_band(ctx, monkeypatch):
     monkeypatch.delenv("WCGH_DIRECT_RU")
     full = stages.synth_points(pts, LAYERS, NH)
     assert np.array_equal(full[700:764], out["2", "2"])
+
+
+# other geometries: the config-3/4 optics (4 um pitch, two of the config-3
+# depths) on a 4096-wide plane with points over its central 2048 columns;
+# a 10 um pitch at z = 0.3 m; and a coarse 20 um pitch at z = 0.2 m whose
+# non-paraxial curvature is too strong for the 16-pixel runs (third
+# difference ~2e-4 rad at the corner), where every requested form must fall
+# back to the per-pixel kernel (bitwise the same plane)
+GEOMS = {
+    "cfg34_optics": (4096, [(WL, 4e-6, 0.15), (WL, 4e-6, 0.30)], 1024, (0, 2047, 4095)),
+    "pitch10_z03": (1024, [(WL, 10e-6, 0.3)], 300, (0, 500, 1023)),
+    "coarse_pitch_fallback": (1024, [(WL, 20e-6, 0.2)], 300, (0, 500, 1023)),
+}
+
+
+def _geom_points(nh, layers, half):
+    rng = np.random.default_rng(77)
+    n = 2500
+    pts = np.zeros(n, _lib.POINT_DTYPE)
+    pts["x"] = rng.integers(nh // 2 - half, nh // 2 + half, n)
+    pts["y"] = rng.integers(nh // 2 - half, nh // 2 + half, n)
+    pts["a"] = rng.integers(1, 256, n).astype(np.float32)
+    pts["layer"] = np.sort(rng.integers(0, len(layers), n))
+    return pts
+
+
+@pytest.mark.parametrize("form", ["0", "1", "2"])
+@pytest.mark.parametrize("geom", sorted(GEOMS))
+def test_direct_forms_other_geometries(ctx, monkeypatch, geom, form):
+    nh, layers, half, rows = GEOMS[geom]
+    pts = _geom_points(nh, layers, half)
+    monkeypatch.setenv("WCGH_DIRECT_REC", form)
+    got = np.stack([stages.synth_points(pts, layers, nh, row0=r, rows=1)[0] for r in rows])
+    py, px = np.meshgrid(np.asarray(rows), np.arange(nh), indexing="ij")
+    ref = O.direct_pixels(pts["x"], pts["y"], pts["a"], pts["layer"], layers, px.ravel(),
+                          py.ravel()).reshape(len(rows), nh)
+    err = O.rel_l2(got, ref)
+    assert err <= 1e-5, (geom, form, err)
+    if geom == "coarse_pitch_fallback":
+        monkeypatch.setenv("WCGH_DIRECT_REC", "0")
+        per_pixel = np.stack([stages.synth_points(pts, layers, nh, row0=r, rows=1)[0] for r in rows])
+        assert np.array_equal(got, per_pixel)
