@@ -479,7 +479,7 @@ template <int NC, int AMP, int MINB, bool CPLX, int RU>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_direct_chirp(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
                  int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
-                 int tiles_x, float2* __restrict__ out, size_t out_chunk_stride) {
+                 int tiles_x, float2* __restrict__ out, size_t out_chunk_stride, int G) {
   constexpr int L = 16;  // run length; 2 runs per thread
   __shared__ int4 sp[kBatch];
   __shared__ float s_tr[256], s_ti[256];
@@ -498,11 +498,23 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int row = ty * 8 + warp;
   const int y = row0 + row;
   const int x0 = tx * 1024 + 32 * lane;
-  const long long p0 = (long long)(chunk0 + blockIdx.y) * kChunk;
-  const long long p1 = min(p0 + kChunk, n_points);
+  // This CTA's partial sums G consecutive 1024-point chunks (G from the
+  // chunk count and the FULL plane size, never the band): each chunk in
+  // registers (fp32), multiplied by Q and added in chunk order into a
+  // per-thread fp32 accumulator in shared memory (16 float4 + 1 pad per
+  // thread: conflict-free); one partial plane per G chunks instead of one
+  // per chunk. The partials are then reduced in fp64 in order as before.
+  extern __shared__ float4 s_acc[];
+  float4* acc = s_acc + size_t(threadIdx.x) * 17;
+  const long long n_chunks = (n_points + kChunk - 1) / kChunk;
+  const long long c_begin = (long long)(chunk0 + blockIdx.y) * G;
+  const long long c_end = min(c_begin + G, n_chunks);
 
   // hr[i] = (re of pixel x0 + i, re of pixel x0 + L + i); hi likewise
   float2 hr[L], hi[L];
+  for (long long cc = c_begin; cc < c_end; ++cc) {
+  const long long p0 = cc * kChunk;
+  const long long p1 = min(p0 + kChunk, n_points);
 #pragma unroll
   for (int i = 0; i < L; ++i) hr[i] = hi[i] = make_float2(0.0f, 0.0f);
 
@@ -664,13 +676,30 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 
   if (cur >= 0) rotate_chirp(hr, hi, cur, -1, s_q);  // H_i = Z_i Q_i
+  if (G > 1) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int p = 2 * m;
+      const float4 r = p < L ? make_float4(hr[p].x, hi[p].x, hr[p + 1].x, hi[p + 1].x)
+                             : make_float4(hr[p - L].y, hi[p - L].y, hr[p - L + 1].y, hi[p - L + 1].y);
+      if (cc == c_begin) {
+        acc[m] = r;
+      } else {
+        const float4 o = acc[m];
+        acc[m] = make_float4(o.x + r.x, o.y + r.y, o.z + r.z, o.w + r.w);
+      }
+    }
+  }
+  }  // chunks
+
   if (row < rows) {
     float2* dst = out + blockIdx.y * out_chunk_stride + size_t(row) * nh;
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       const int p = 2 * m, x = x0 + p;
-      const float4 r = p < L ? make_float4(hr[p].x, hi[p].x, hr[p + 1].x, hi[p + 1].x)
-                             : make_float4(hr[p - L].y, hi[p - L].y, hr[p - L + 1].y, hi[p - L + 1].y);
+      const float4 r = G > 1 ? acc[m]
+                     : (p < L ? make_float4(hr[p].x, hi[p].x, hr[p + 1].x, hi[p + 1].x)
+                              : make_float4(hr[p - L].y, hi[p - L].y, hr[p - L + 1].y, hi[p - L + 1].y));
       WCGH_DCHECK(x >= nh || size_t(blockIdx.y) * out_chunk_stride + size_t(row) * nh + x <
                                  size_t(gridDim.y) * out_chunk_stride);
       if (x + 1 < nh)
@@ -680,7 +709,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
   }
 }
-
 
 // Double-phase option: r and k*r in fp64, reduced to [-pi, pi] in fp64, then
 // fp32 sin/cos. Accuracy mode (FP64-pipe bound).
@@ -813,7 +841,9 @@ struct LaunchArgs {
   int chunk0, nh, row0, rows, tiles_x;
   float2* out;
   size_t stride;
+  int G;  // chunks per partial (k_direct_chirp; 1 for the other forms)
 };
+constexpr size_t kChirpAccBytes = size_t(kThreads) * 17 * sizeof(float4);
 
 int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled, tuning)
   const char* e = std::getenv("WCGH_DIRECT_RU");
@@ -824,10 +854,17 @@ template <int NC, int AMP>
 void launch_rec(const LaunchArgs& a, bool chirp) {
   constexpr int MINB = 2;
 #define WCGH_REC(CPLX_, RU_)                                                              \
-  if (chirp)                                                                              \
-    k_direct_chirp<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(             \
-        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride); \
-  else                                                                                    \
+  if (chirp) {                                                                            \
+    const size_t dyn = a.G > 1 ? kChirpAccBytes : 0;                                      \
+    /* per device and cheap: set on every launch (multi-device callers) */                 \
+    if (dyn)                                                                              \
+      WCGH_CUDA(cudaFuncSetAttribute(k_direct_chirp<NC, AMP, MINB, CPLX_, RU_>,           \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                     int(kChirpAccBytes)));                                \
+    k_direct_chirp<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, dyn, a.s>>>(           \
+        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride, \
+        a.G);                                                                             \
+  } else                                                                                  \
     k_direct_rec<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(               \
         a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride)
   const bool u2 = rec_unroll() == 2;
@@ -896,6 +933,17 @@ void launch_fixed_nc(const DirectPlan& plan, const LaunchArgs& a) {
     launch_fixed_amp<P, 5>(plan, a);
   else
     launch_fixed_amp<P, 8>(plan, a);
+}
+
+// k_direct_chirp: 1024-point chunks per CTA (one partial plane each). The
+// full plane's (tile, chunk) work divided by 16384 CTAs, clamped to 1..64:
+// config 4 (1252 chunks, 2048 tiles) -> 64 (20 partial planes instead of
+// 1252), config 1 (81 chunks, 128 tiles) -> 1. WCGH_DIRECT_G overrides.
+int chirp_chunks_per_cta(int n_chunks, int nh) {
+  if (const char* e = std::getenv("WCGH_DIRECT_G")) return std::max(1, std::atoi(e));
+  const long long tiles_full = (long long)((nh + 1023) / 1024) * ((nh + 7) / 8);
+  const long long g = (long long)n_chunks * tiles_full / 16384;
+  return int(std::max(1LL, std::min(64LL, g)));
 }
 
 int pixels_per_thread(int nh) {
@@ -1062,7 +1110,12 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
                                     cudaMemcpyHostToDevice, stream));
 
   const int n_chunks = int((n_points + kChunk - 1) / kChunk);
-  const int group = partial_group(n_chunks, nh);
+  // chunks per partial plane: 1, or for the chirp form G from the chunk count
+  // and the full plane's tile count (never the band), so the fp32 grouping
+  // and hence every bit of the plane is the same for any row-band split
+  const int G = phase_mode == WCGH_PHASE_FIXED && plan.rec == 2 ? chirp_chunks_per_cta(n_chunks, nh) : 1;
+  const int n_parts = (n_chunks + G - 1) / G;
+  const int group = partial_group(n_parts, nh);
   const int P = pixels_per_thread(nh);
   const int tiles_x = (nh + 32 * P - 1) / (32 * P);
   const int tiles_y = (rows + 7) / 8;
@@ -1083,11 +1136,11 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
   static_assert(sizeof(long long) == sizeof(int64_t), "int64");
   WCGH_CUDA(cudaMemcpyAsync(lb_dev, layer_begin_host, lb_bytes, cudaMemcpyHostToDevice, stream));
 
-  for (int g0 = 0; g0 < n_chunks; g0 += group) {
-    const int ng = std::min(group, n_chunks - g0);
+  for (int g0 = 0; g0 < n_parts; g0 += group) {
+    const int ng = std::min(group, n_parts - g0);
     LaunchArgs a{dim3(unsigned(tiles_x * tiles_y), unsigned(ng)), stream,
                  pts, pim_dev != nullptr, lb_dev, n_layers, n_points, g0, nh,
-                 row0, rows, tiles_x, partial, band};
+                 row0, rows, tiles_x, partial, band, G};
     if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), stream));
     if (phase_mode == WCGH_PHASE_FP64) {
       if (P == 32)
@@ -1108,7 +1161,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     }
     WCGH_CHECK_LAUNCH();
     if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), stream));
-    const bool last = g0 + ng >= n_chunks;
+    const bool last = g0 + ng >= n_parts;
     const PeerPlanes pp = last && peers ? *peers : PeerPlanes{};
     if (band % 2 == 0 && reinterpret_cast<uintptr_t>(out_dev) % 16 == 0 && peers_aligned16(pp))
       k_reduce_chunks2<<<unsigned((band / 2 + 255) / 256), 256, 0, stream>>>(

@@ -129,3 +129,27 @@ def test_direct_forms_other_geometries(ctx, monkeypatch, geom, form):
         monkeypatch.setenv("WCGH_DIRECT_REC", "0")
         per_pixel = np.stack([stages.synth_points(pts, layers, nh, row0=r, rows=1)[0] for r in rows])
         assert np.array_equal(got, per_pixel)
+
+
+def test_chirp_chunk_groups_band_invariant(ctx, monkeypatch):
+    """k_direct_chirp sums G consecutive 1024-point chunks per partial plane
+    (fp32 in shared memory, in chunk order; G from the chunk count and the
+    full plane, never the band). Forcing G = 3 on 3000 points / 2 layers
+    (3 chunks, one partial, a layer switch inside): the plane matches G = 1
+    to the fp32 level, against the fp64 oracle as well, and any row band is
+    bitwise the same rows of the full plane."""
+    pts = _points()
+    monkeypatch.setenv("WCGH_DIRECT_REC", "2")
+    monkeypatch.setenv("WCGH_DIRECT_G", "1")
+    g1 = stages.synth_points(pts, LAYERS, NH)
+    monkeypatch.setenv("WCGH_DIRECT_G", "3")
+    g3 = stages.synth_points(pts, LAYERS, NH)
+    assert O.rel_l2(g3, g1) <= 1e-6
+    ref = _oracle_rows(pts, ROWS)
+    assert O.rel_l2(g3[list(ROWS)], ref) <= 1e-5
+    for r0, r1 in ((0, 8), (700, 764), (1492, 1500), (13, 1111)):
+        band = stages.synth_points(pts, LAYERS, NH, row0=r0, rows=r1 - r0)
+        assert np.array_equal(band, g3[r0:r1]), (r0, r1)
+    monkeypatch.setenv("WCGH_DIRECT_G", "2")  # 2 partials, the last one short
+    g2 = stages.synth_points(pts, LAYERS, NH)
+    assert O.rel_l2(g2, g1) <= 1e-6

@@ -14,6 +14,7 @@ import bench  # noqa: E402
 from paper_2211_09938_b200 import scenes  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+estimate_only = "--estimate-only" in sys.argv
 sc = scenes.make_scene(cfg)
 t = bench.ReferenceTimer(sc)
 try:
@@ -21,7 +22,7 @@ try:
     est, desc = t.estimate(10.0)
     t_est = time.perf_counter() - t0
     t1 = time.perf_counter()
-    full, fdesc = t.full()
+    full, fdesc = (float("nan"), "") if estimate_only else t.full()
     t_full = time.perf_counter() - t1
 finally:
     t.close()
