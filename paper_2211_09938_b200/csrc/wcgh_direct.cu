@@ -846,8 +846,7 @@ struct LaunchArgs {
 constexpr size_t kChirpAccBytes = size_t(kThreads) * 17 * sizeof(float4);
 
 int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled, tuning)
-  const char* e = std::getenv("WCGH_DIRECT_RU");
-  return e && std::atoi(e) == 1 ? 1 : 2;
+  return env_int("WCGH_DIRECT_RU", 2) == 1 ? 1 : 2;
 }
 
 template <int NC, int AMP>
@@ -940,7 +939,7 @@ void launch_fixed_nc(const DirectPlan& plan, const LaunchArgs& a) {
 // config 4 (1252 chunks, 2048 tiles) -> 64 (20 partial planes instead of
 // 1252), config 1 (81 chunks, 128 tiles) -> 1. WCGH_DIRECT_G overrides.
 int chirp_chunks_per_cta(int n_chunks, int nh) {
-  if (const char* e = std::getenv("WCGH_DIRECT_G")) return std::max(1, std::atoi(e));
+  if (const int g = env_int("WCGH_DIRECT_G", 0); g > 0) return g;
   const long long tiles_full = (long long)((nh + 1023) / 1024) * ((nh + 7) / 8);
   const long long g = (long long)n_chunks * tiles_full / 16384;
   return int(std::max(1LL, std::min(64LL, g)));
@@ -948,10 +947,7 @@ int chirp_chunks_per_cta(int n_chunks, int nh) {
 
 int pixels_per_thread(int nh) {
   // WCGH_DIRECT_P (16 or 32, nh >= 1024 only) overrides: tuning experiments
-  static const int forced = [] {
-    const char* e = std::getenv("WCGH_DIRECT_P");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int forced = env_int("WCGH_DIRECT_P", 0);
   if (nh >= 1024 && (forced == 16 || forced == 32)) return forced;
   return nh >= 1024 ? 32 : (nh >= 512 ? 16 : 4);
 }
@@ -1052,7 +1048,7 @@ DirectPlan plan_direct(const wcgh_layer* layers, int n_layers, double max_dx, do
   plan.amp_degree = amp_rsqrt ? 0 : (amp3 ? 3 : (amp2 ? 2 : 1));
   // WCGH_DIRECT_AMP (0..3) forces the amplitude series degree: tuning
   // experiments only (it can exceed the 2e-6 truncation budget)
-  if (const char* e = std::getenv("WCGH_DIRECT_AMP")) plan.amp_degree = std::max(0, std::min(3, std::atoi(e)));
+  if (const int a = env_int("WCGH_DIRECT_AMP", -1); a >= 0) plan.amp_degree = std::min(3, a);
   return plan;
 }
 
@@ -1084,8 +1080,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     // differences, see k_direct_rec). WCGH_DIRECT_REC selects the form for
     // comparisons: 0 per-pixel (k_direct_fixed), 1 k_direct_rec, 2 (default)
     // the chirp-factored k_direct_chirp.
-    const char* rec_e = std::getenv("WCGH_DIRECT_REC");  // read per call (tests switch it)
-    const int rec_env = rec_e ? std::atoi(rec_e) : 2;
+    const int rec_env = env_int("WCGH_DIRECT_REC", 2);  // read per call (tests switch it)
     // The runs neglect the correction's third difference (phase error <=
     // L^3/12 * phi''' at the run end, phi''' ~ 3 G c^2 |dx|) and the chirp
     // form linearises the multiplier (error ~ C(L-1, 2) dc^2, dc ~ G c^2

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +34,12 @@ struct RuntimeError : std::runtime_error {
 
 inline void require(bool ok, const std::string& what) {
   if (!ok) throw ValidationError(what);
+}
+
+// Tuning / test overrides from the environment: unset or empty = default.
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
 }
 
 // ---- checked build (-DWCGH_CHECKED, libwcgh_checked.so; test use only) -------

@@ -362,7 +362,7 @@ struct LutVariant {
 LutVariant lut_variant() {
   static const LutVariant v = [] {
     LutVariant d{8, 2, 2, 4};
-    if (const char* e = std::getenv("WCGH_LUT_VARIANT")) {
+    if (const char* e = std::getenv("WCGH_LUT_VARIANT"); e && *e) {
       int r = 0, px = 0, dd = 0, w = 4;
       const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
       if (got >= 3) d = LutVariant{r, px, dd, w};
@@ -374,17 +374,11 @@ LutVariant lut_variant() {
 // Largest gap (in cell rows) a run steps through with zero weights; a wider
 // gap starts a new run (window reload). WCGH_LUT_GAP overrides (tuning).
 int lut_gap() {
-  static const int g = [] {
-    const char* e = std::getenv("WCGH_LUT_GAP");
-    return e ? std::max(1, std::atoi(e)) : lut_variant().R;
-  }();
+  static const int g = std::max(1, env_int("WCGH_LUT_GAP", lut_variant().R));
   return g;
 }
 int lut_chunk_target() {
-  static const int t = [] {
-    const char* e = std::getenv("WCGH_LUT_CHUNKS");
-    return e ? std::max(1, std::atoi(e)) : 8;
-  }();
+  static const int t = std::max(1, env_int("WCGH_LUT_CHUNKS", 8));
   return t;
 }
 
