@@ -153,3 +153,33 @@ def test_chirp_chunk_groups_band_invariant(ctx, monkeypatch):
     monkeypatch.setenv("WCGH_DIRECT_G", "2")  # 2 partials, the last one short
     g2 = stages.synth_points(pts, LAYERS, NH)
     assert O.rel_l2(g2, g1) <= 1e-6
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_direct_random_geometries(ctx, case):
+    """Seeded random optics and plane sizes through the default planner
+    (per-pixel, or the chirp recurrence when its curvature bounds hold):
+    the result meets the 1e-4 bar with a 10x margin against the fp64
+    Eq.(1) oracle on three rows."""
+    rng = np.random.default_rng(1000 + case)
+    nh = int(rng.choice([1024, 1536, 2048, 3000]))
+    pitch = float(rng.uniform(2e-6, 12e-6))
+    zs = sorted(float(z) for z in rng.uniform(0.1, 0.5, int(rng.integers(1, 3))))
+    layers = [(WL, pitch, z) for z in zs]
+    n = int(rng.integers(500, 2500))
+    half = int(rng.integers(64, nh // 3))
+    pts = np.zeros(n, _lib.POINT_DTYPE)
+    pts["x"] = rng.integers(nh // 2 - half, nh // 2 + half, n)
+    pts["y"] = rng.integers(nh // 2 - half, nh // 2 + half, n)
+    pts["a"] = rng.integers(1, 256, n).astype(np.float32)
+    pts["layer"] = np.sort(rng.integers(0, len(layers), n))
+    rows = (0, int(rng.integers(1, nh - 1)), nh - 1)
+    try:
+        got = np.stack([stages.synth_points(pts, layers, nh, row0=r, rows=1)[0] for r in rows])
+    except _lib.ValidationError:
+        pytest.skip("geometry too oblique for the fixed-point phase (rejected by design)")
+    py, px = np.meshgrid(np.asarray(rows), np.arange(nh), indexing="ij")
+    ref = O.direct_pixels(pts["x"], pts["y"], pts["a"], pts["layer"], layers, px.ravel(),
+                          py.ravel()).reshape(len(rows), nh)
+    err = O.rel_l2(got, ref)
+    assert err <= 1e-5, (case, nh, pitch, zs, err)
