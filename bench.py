@@ -48,6 +48,7 @@ CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
 # NC = 2) + ~12 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
 K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
 K3_LANE_OPS_PER_UPDATE = 10.0
+FFMA2_CEILING_LANE_FMA_PER_CLK = 111.0  # measured, profiles/s3_microbench_fmamix.txt
 # one whole reference hologram at a 4096^2 config, timed on the GPU box's
 # host against the extrapolation model (tools/ref_full_check.py)
 REF_FULL_CHECK = ("config 4 whole reference synthesize_progressive on 16 host cores: 1361 s "
@@ -557,6 +558,13 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
         roof["traffic_note"] = ("dram__bytes_read+write per K3/K4 launch from one `ncu --set full` "
                                 "capture; dominated by the fixed-order fp32 partial-sum planes "
                                 "(compute-bound kernel, < 1% DRAM utilisation)")
+    if bound == "fp32" and achieved:
+        # the packed-FFMA2 ceiling measured by tools/microbench_fmamix.cu on this
+        # pool (16 independent accumulators, no loads): 111 of 128 lane-FMA/clk/SM
+        ceil = SM_COUNT * f_max * FFMA2_CEILING_LANE_FMA_PER_CLK / 2.0
+        roof["measured_ffma2_ceiling"] = ceil
+        roof["frac_of_measured_ffma2_ceiling"] = achieved / ceil
+        roof["ffma2_ceiling_source"] = "profiles/s3_microbench_fmamix.txt"
     if bound == "sfu" and achieved:
         fp32_peak = SM_COUNT * f_max * 128.0 / K3_LANE_OPS_PER_UPDATE
         roof["fp32_bound"] = fp32_peak
