@@ -44,8 +44,8 @@ SM_COUNT = 148
 MUFU_PER_CLK_SM = 16.0
 CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
 # K3 as built (k_direct_chirp, point loop unrolled by 2): per point and thread
-# (32 updates) 158 packed fp32x2 FMA-pipe instructions (config 4, NC = 3; 155 at
-# NC = 2) + ~12 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
+# (32 updates) 154 packed fp32x2 FMA-pipe instructions (config 4, NC = 3) +
+# ~10 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
 K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
 K3_LANE_OPS_PER_UPDATE = 10.0
 FFMA2_CEILING_LANE_FMA_PER_CLK = 111.0  # measured, profiles/s3_microbench_fmamix.txt
