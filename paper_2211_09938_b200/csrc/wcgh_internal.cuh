@@ -442,9 +442,17 @@ struct StageCells {
   int gap = 0;  // run gap threshold (the window height R) the lists were built with
   int n_runs = 0, n_dense = 0, nnz = 0;
   DevBuf counts, offsets, runs, dense;
+  // host copies of the run list (the K4 chunk kernel takes each chunk's runs
+  // and weights as a kernel parameter block); valid after stage_cells_fetch
+  bool host_valid = false;
+  std::vector<int4> h_runs;
+  std::vector<float> h_dense;
 };
 int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t stream);
 void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t stream);
+// Copies the run list (n_runs, n_dense filled) to the host; blocks until the
+// stream has produced it.
+void stage_cells_fetch(StageCells& sc, cudaStream_t stream);
 // out (rows x nh complex64, overwritten) = superposition of the stage's
 // listed cells with the block-B LUT; object grid offset `off` on the plane.
 // accumulate: out += instead; rotate: out += i * superposition (the

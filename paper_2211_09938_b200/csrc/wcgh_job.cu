@@ -359,6 +359,22 @@ void run_job_lut(wcgh_job* j, cudaStream_t s, bool synth) {
     j->stats.ms_total = j->stats.ms_analysis;
     return;
   }
+  // the K4 chunk kernel takes the run lists as parameter blocks: one copy of
+  // every stage's list to the host while the stream is idle
+  for (int k = 0; k < 4 * L; ++k) {
+    StageCells& sc = *j->cells[k];
+    sc.n_runs = j->h_tot[3 * k];
+    sc.n_dense = j->h_tot[3 * k + 1];
+    sc.nnz = j->h_tot[3 * k + 2];
+    stage_cells_fetch(sc, s);
+    if (cplx) {
+      StageCells& si = *j->cells_im[k];
+      si.n_runs = h_tot_im[3 * k];
+      si.n_dense = h_tot_im[3 * k + 1];
+      si.nnz = h_tot_im[3 * k + 2];
+      stage_cells_fetch(si, s);
+    }
+  }
   const size_t band = size_t(d.rows) * d.plane_size;
   float2* sp = j->stage_planes.as<float2>();
   long long cells = 0;

@@ -34,6 +34,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <memory>
 #include <vector>
 
 #include "wcgh_internal.cuh"
@@ -323,6 +325,130 @@ __global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
   }
 }
 
+// One chunk of a stage's run list as a kernel parameter block (the default
+// K4 form). The weights then come from the constant bank through uniform
+// registers (LDCU), and an FFMA2 whose scalar operand is a uniform register
+// reads only its two register pairs: one even and one odd register each, so
+// it issues at the pipe rate. With the weight in a regular register (the
+// shared-memory form above) the third read conflicts in the register banks
+// whenever the operand-reuse cache misses: tools/microbench_operands.cu
+// measures 125-127 lane-FMA/clk/SM for the uniform/constant operand against
+// 110-111 for the register operand (128 = the FP32 pipe).
+//   d[2i]     = c_x | c_y << 16      (run i: cell column, first cell row)
+//   d[2i + 1] = steps | woff << 16   (its step count, first weight at d[w_base + woff])
+//   d[w_base ...] = the dense per-step weights (zeros in gaps), then >= S zeros.
+constexpr int kChunkInts = 8160;
+struct LutChunk {
+  int n_runs;
+  int w_base;
+  int d[kChunkInts];
+};
+static_assert(sizeof(LutChunk) + 64 <= 32764, "kernel parameter space");
+
+template <int B, int R, int PX, int D, int W>
+__global__ void __launch_bounds__(W * 32, lut_min_blocks(R, PX, D, W))
+    k_lut_chunk(const float2* __restrict__ lut, int nh, int off, int row0, int rows, int tiles_x,
+                float2* __restrict__ out, const __grid_constant__ LutChunk ck) {
+  constexpr int S = R + D;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = blockIdx.x % tiles_x, tyc = blockIdx.x / tiles_x;
+  const int r = tyc % B;
+  const int g = (tyc / B) * W + warp;
+  const int yb = g * (B * R) + r;
+  const int x0 = tx * (32 * PX) + lane;
+  const int span = 2 * nh - 1;
+#ifdef WCGH_CHECKED
+  const float2* lut_lo = lut - size_t(kLutGuardBefore) * span;
+  const float2* lut_hi = lut + size_t(span + kLutGuardAfter) * span + kLutPadCols;
+#define WCGH_LUT_IN(ptr) WCGH_DCHECK((ptr) >= lut_lo && (ptr) + 32 * (PX - 1) < lut_hi)
+#else
+#define WCGH_LUT_IN(ptr)
+#endif
+  float2 acc[R][PX];
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int i = 0; i < PX; ++i) acc[j][i] = make_float2(0.f, 0.f);
+
+  const int rho_base = row0 + yb - off + nh - 1;
+  const long long row_step = (long long)B * span;
+  for (int ri = 0; ri < ck.n_runs; ++ri) {
+    const unsigned rx = unsigned(ck.d[2 * ri]), ry = unsigned(ck.d[2 * ri + 1]);
+    const int cx = int(rx & 0xffffu), cy_s = int(rx >> 16), n_steps = int(ry & 0xffffu);
+    const int wo = ck.w_base + int(ry >> 16);
+    WCGH_DCHECK(wo + n_steps + S - 1 <= kChunkInts);
+    const float2* rp = lut + (x0 - off - B * cx + nh - 1) + (long long)(rho_base - B * cy_s) * span;
+    float2 ring[S][PX];
+    {
+      const float2* rt = rp - D * row_step;
+#pragma unroll
+      for (int t = -D; t < R; ++t) {
+        WCGH_LUT_IN(rt);
+#pragma unroll
+        for (int i = 0; i < PX; ++i) ring[(t + S) % S][i] = __ldg(rt + 32 * i);
+        rt += row_step;
+      }
+    }
+    const float2* pf = rp - (D + 1) * row_step;
+    // one step: MAC the listed weight (zeros in gaps are multiplied, not
+    // predicated: a predicated-off FFMA2 occupies the pipe all the same, and
+    // the predicate would need the weight in a regular register)
+#define WCGH_LUT_STEP_W(uu, wexpr)                                              \
+  {                                                                             \
+    const float wv = (wexpr);                                                   \
+    _Pragma("unroll") for (int j = 0; j < R; ++j)                               \
+    _Pragma("unroll") for (int i = 0; i < PX; ++i) {                            \
+      acc[j][i] = ffma2(wv, ring[(j - (uu) + 2 * S) % S][i], acc[j][i]);        \
+    }                                                                           \
+    WCGH_LUT_IN(pf);                                                            \
+    _Pragma("unroll") for (int i = 0; i < PX; ++i)                              \
+      ring[(R - 1 - (uu) + S) % S][i] = __ldg(pf + 32 * i);                     \
+    pf -= row_step;                                                             \
+  }
+    const int full = n_steps - n_steps % S;
+    for (int ub = 0; ub < full; ub += S) {
+#pragma unroll
+      for (int uu = 0; uu < S; ++uu) WCGH_LUT_STEP_W(uu, __int_as_float(ck.d[wo + ub + uu]))
+    }
+    const int rem = n_steps - full;
+    if (rem > 0) {
+      // the parameter block holds >= S zero weights past its last run
+      constexpr int T1 = (S - 1) / 3, T2 = 2 * (S - 1) / 3;
+      const int wr = wo + full;
+      if (rem <= T1) {
+#pragma unroll
+        for (int uu = 0; uu < T1; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, __int_as_float(ck.d[wr + uu]))
+        }
+      } else if (rem <= T2) {
+#pragma unroll
+        for (int uu = 0; uu < T2; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, __int_as_float(ck.d[wr + uu]))
+        }
+      } else {
+#pragma unroll
+        for (int uu = 0; uu < S - 1; ++uu) {
+          if (uu < rem) WCGH_LUT_STEP_W(uu, __int_as_float(ck.d[wr + uu]))
+        }
+      }
+    }
+#undef WCGH_LUT_STEP_W
+  }
+#undef WCGH_LUT_IN
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int row = yb + j * B;
+    if (row < rows) {
+      float2* dst = out + size_t(row) * nh;
+#pragma unroll
+      for (int i = 0; i < PX; ++i) {
+        const int x = x0 + 32 * i;
+        if (x < nh) dst[x] = acc[j][i];
+      }
+    }
+  }
+}
+
 // out (+)= sum of `n` partial planes in order, fp64 accumulation. rotate:
 // out += i * sum (imaginary LUT weights of a complex object).
 __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, size_t count,
@@ -413,6 +539,160 @@ void launch_stage_b(const LutVariant& v, const float2* lut, int nh, const StageC
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled");
 }
 
+template <int B, int R, int PX, int D, int W>
+void launch_chunk_v(const float2* lut, int nh, int off, int row0, int rows, int tiles_x, int grid,
+                    float2* out, const LutChunk& ck, cudaStream_t s) {
+  k_lut_chunk<B, R, PX, D, W><<<grid, W * 32, 0, s>>>(lut, nh, off, row0, rows, tiles_x, out, ck);
+}
+
+template <int B>
+void launch_chunk_b(const LutVariant& v, const float2* lut, int nh, int off, int row0, int rows,
+                    int tiles_x, int grid, float2* out, const LutChunk& ck, cudaStream_t s) {
+#define WCGH_V(R_, PX_, D_, W_)                                                                \
+  if (v.R == R_ && v.PX == PX_ && v.D == D_ && v.W == W_) {                                    \
+    launch_chunk_v<B, R_, PX_, D_, W_>(lut, nh, off, row0, rows, tiles_x, grid, out, ck, s);   \
+    return;                                                                                    \
+  }
+  WCGH_V(8, 2, 2, 4)
+  WCGH_V(8, 2, 1, 4)
+  WCGH_V(8, 2, 3, 4)
+  WCGH_V(16, 2, 2, 4)
+#undef WCGH_V
+  throw ValidationError("WCGH_LUT_VARIANT: shape not compiled for the chunk kernel");
+}
+
+// K4 form: 1 = run-list chunks as kernel parameter blocks (default), 0 = the
+// shared-memory form (weights staged per CTA, predicated zero steps).
+bool lut_params() {
+  static const bool p = env_int("WCGH_LUT_PARAMS", 1) != 0;
+  return p;
+}
+
+// Side streams the chunk launches of one stage are spread over, so that a
+// launch's last partial wave overlaps the next launch (per host thread and
+// device; created once).
+constexpr int kSideStreams = 4;
+struct SideStreams {
+  int dev = -1;
+  cudaStream_t st[kSideStreams];
+  cudaEvent_t fork, join[kSideStreams];
+};
+SideStreams& side_streams() {
+  thread_local std::vector<std::unique_ptr<SideStreams>> pools;
+  int dev = 0;
+  WCGH_CUDA(cudaGetDevice(&dev));
+  for (auto& p : pools)
+    if (p->dev == dev) return *p;
+  auto p = std::make_unique<SideStreams>();
+  p->dev = dev;
+  for (int k = 0; k < kSideStreams; ++k) {
+    WCGH_CUDA(cudaStreamCreateWithFlags(&p->st[k], cudaStreamNonBlocking));
+    WCGH_CUDA(cudaEventCreateWithFlags(&p->join[k], cudaEventDisableTiming));
+  }
+  WCGH_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+  pools.push_back(std::move(p));
+  return *pools.back();
+}
+
+// Splits a stage's run list into parameter blocks, in list order. A chunk
+// closes once it holds `target` weights (so a stage has >= kMinChunks chunks
+// to spread over the side streams) or when the next record would not fit;
+// a run longer than the room left is split (its remainder restarts the
+// window at the next cell row). Depends on the run list only, never on the
+// row band, so the partial planes and their reduction are band-invariant.
+constexpr int kMinChunks = 4;
+void build_chunks(const StageCells& sc, int S, std::vector<LutChunk>& out) {
+  out.clear();
+  const int cap = kChunkInts - S;  // records + weights (S zero weights of slack after)
+  const int target =
+      std::min(cap, std::max(16 * S, (sc.n_dense + kMinChunks - 1) / kMinChunks));
+  std::vector<int> recs;
+  std::vector<float> ws;
+  auto flush = [&] {
+    if (recs.empty()) return;
+    out.emplace_back();
+    LutChunk& c = out.back();
+    const int nr = int(recs.size() / 2);
+    c.n_runs = nr;
+    c.w_base = 2 * nr;
+    std::copy(recs.begin(), recs.end(), c.d);
+    std::memcpy(c.d + c.w_base, ws.data(), ws.size() * sizeof(float));
+    std::fill(c.d + c.w_base + ws.size(), c.d + kChunkInts, 0);
+    recs.clear();
+    ws.clear();
+  };
+  for (int i = 0; i < sc.n_runs; ++i) {
+    const int4 run = sc.h_runs[size_t(i)];
+    int cy = run.y, n = run.z;
+    size_t wofs = size_t(run.w);
+    require(run.x < 65536 && cy + n <= 65536, "LUT superposition: cell grid too large");
+    while (n > 0) {
+      if (int(ws.size()) >= target) flush();
+      const int room = cap - int(recs.size()) - 2 - int(ws.size());
+      if (room < std::min(n, S) && !recs.empty()) {
+        flush();
+        continue;
+      }
+      const int take = std::min(n, room);
+      recs.push_back(run.x | (cy << 16));
+      recs.push_back(take | (int(ws.size()) << 16));
+      ws.insert(ws.end(), sc.h_dense.begin() + wofs, sc.h_dense.begin() + wofs + take);
+      cy += take;
+      wofs += size_t(take);
+      n -= take;
+    }
+  }
+  flush();
+}
+
+int launch_lut_chunks(const float2* lut, int nh, int block, const StageCells& sc, int off,
+                      int row0, int rows, float2* out, DevBuf& partial, cudaStream_t s,
+                      DirectTiming* timing, bool accumulate, bool rotate) {
+  const LutVariant v = lut_variant();
+  thread_local std::vector<LutChunk> chunks;
+  build_chunks(sc, v.R + v.D, chunks);
+  const size_t band = size_t(rows) * nh;
+  const int n_chunks = int(chunks.size());
+  const int group = partial_group(n_chunks, nh);
+  float2* part = static_cast<float2*>(partial.reserve(band * group * sizeof(float2)));
+  const int tiles_x = (nh + 32 * v.PX - 1) / (32 * v.PX);
+  const int groups = (rows + block * v.R - 1) / (block * v.R);
+  const int tiles_y = block * ((groups + v.W - 1) / v.W);
+  const int grid = tiles_x * tiles_y;
+  SideStreams& ss = side_streams();
+  int launches = 0;
+  for (int g0 = 0; g0 < n_chunks; g0 += group) {
+    const int ng = std::min(group, n_chunks - g0);
+    const int nside = std::min(ng, kSideStreams);
+    if (timing) WCGH_CUDA(cudaEventRecord(timing->begin(), s));
+    WCGH_CUDA(cudaEventRecord(ss.fork, s));
+    for (int k = 0; k < nside; ++k) WCGH_CUDA(cudaStreamWaitEvent(ss.st[k], ss.fork, 0));
+    for (int c = 0; c < ng; ++c) {
+      cudaStream_t sk = ss.st[c % nside];
+      float2* o = part + band * size_t(c);
+      const LutChunk& ck = chunks[size_t(g0 + c)];
+      switch (block) {
+        case 1: launch_chunk_b<1>(v, lut, nh, off, row0, rows, tiles_x, grid, o, ck, sk); break;
+        case 2: launch_chunk_b<2>(v, lut, nh, off, row0, rows, tiles_x, grid, o, ck, sk); break;
+        case 4: launch_chunk_b<4>(v, lut, nh, off, row0, rows, tiles_x, grid, o, ck, sk); break;
+        case 8: launch_chunk_b<8>(v, lut, nh, off, row0, rows, tiles_x, grid, o, ck, sk); break;
+        default: throw ValidationError("LUT superposition: unsupported block size");
+      }
+      WCGH_CHECK_LAUNCH();
+    }
+    for (int k = 0; k < nside; ++k) {
+      WCGH_CUDA(cudaEventRecord(ss.join[k], ss.st[k]));
+      WCGH_CUDA(cudaStreamWaitEvent(s, ss.join[k], 0));
+    }
+    if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
+    k_reduce_partials<<<unsigned((band + 255) / 256), 256, 0, s>>>(part, ng, band,
+                                                                  accumulate || g0 > 0, rotate, out);
+    WCGH_CHECK_LAUNCH();
+    launches += ng + 1;
+  }
+  return launches;
+}
+
 }  // namespace
 
 int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, DevBuf& scratch,
@@ -435,6 +715,7 @@ int launch_build_lut(const wcgh_layer& scene, int n, int block, float2* lut, Dev
 
 int launch_stage_cells(const float* w, int m, StageCells& sc, cudaStream_t s) {
   sc.m = m;
+  sc.host_valid = false;
   int* c = static_cast<int*>(sc.counts.reserve(sizeof(int) * 3 * (size_t(m) + 1)));
   int* o = static_cast<int*>(sc.offsets.reserve(sizeof(int) * 3 * (size_t(m) + 1)));
   const size_t mm = size_t(m) * m;
@@ -459,6 +740,19 @@ void stage_cells_totals_async(const StageCells& sc, int* host3, cudaStream_t s) 
     WCGH_CUDA(cudaMemcpyAsync(host3 + k, o + k * (m + 1) + m, sizeof(int), cudaMemcpyDeviceToHost, s));
 }
 
+void stage_cells_fetch(StageCells& sc, cudaStream_t s) {
+  sc.h_runs.resize(size_t(sc.n_runs));
+  sc.h_dense.resize(size_t(sc.n_dense));
+  if (sc.n_runs > 0) {
+    WCGH_CUDA(cudaMemcpyAsync(sc.h_runs.data(), sc.runs.p, sizeof(int4) * size_t(sc.n_runs),
+                              cudaMemcpyDeviceToHost, s));
+    WCGH_CUDA(cudaMemcpyAsync(sc.h_dense.data(), sc.dense.p, sizeof(float) * size_t(sc.n_dense),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  WCGH_CUDA(cudaStreamSynchronize(s));
+  sc.host_valid = true;
+}
+
 int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int off, int row0,
                      int rows, float2* out, DevBuf& partial, cudaStream_t s, DirectTiming* timing,
                      bool accumulate, bool rotate) {
@@ -473,6 +767,11 @@ int launch_lut_stage(const float2* lut, int nh, int block, StageCells& sc, int o
   require(sc.gap >= 1, "LUT superposition: run lists not built");
   require(block * v.R * v.W <= kLutGuardAfter - 16 && block * (v.D + 1) + 1 <= kLutGuardBefore,
           "LUT superposition: window shape exceeds the LUT guard rows");
+  if (lut_params()) {
+    if (!sc.host_valid) stage_cells_fetch(sc, s);
+    return launch_lut_chunks(lut, nh, block, sc, off, row0, rows, out, partial, s, timing,
+                             accumulate, rotate);
+  }
   const int target = lut_chunk_target();
   int chunk_steps = std::min(kMaxChunkSteps, std::max(256, (sc.n_dense + target - 1) / target));
   chunk_steps = (chunk_steps + 127) / 128 * 128;
