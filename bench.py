@@ -48,7 +48,10 @@ CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
 # ~10 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
 K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
 K3_LANE_OPS_PER_UPDATE = 10.0
-FFMA2_CEILING_LANE_FMA_PER_CLK = 111.0  # measured, profiles/s3_microbench_fmamix.txt
+# packed FFMA2 with the scalar operand in a uniform register (K4's parameter-block form),
+# measured by tools/microbench_operands.cu: profiles/s4_microbench_operands.txt (116 of 128;
+# 111 with the weight in a regular register, 125-127 straight from the constant bank)
+FFMA2_CEILING_LANE_FMA_PER_CLK = 116.0
 # one whole reference hologram at a 4096^2 config, timed on the GPU box's
 # host against the extrapolation model (tools/ref_full_check.py)
 REF_FULL_CHECK = ("config 4 whole reference synthesize_progressive on 16 host cores: 1361 s "
@@ -521,10 +524,11 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
         bound, key = "sfu", "k_direct_chirp"
         dram = int(points * 16 + rows * c.plane_size * 8)
     elif job.spec.method == "lut":
-        per_clk, kernel = 128.0 / 2.0, "k_lut_stage (K4), 4 stage launches"
+        per_clk, kernel = 128.0 / 2.0, ("k_lut_chunk (K4): run-list chunks of the 4 stages as kernel "
+                           "parameter blocks, 16x2 register window")
         basis = (f"FP32 roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz x 128 FFMA/clk/SM / 2 FFMA per "
                  "(nonzero cell, pixel) update (SURVEY.md §8(d))")
-        bound, key = "fp32", "k_lut_stage"
+        bound, key = "fp32", "k_lut_chunk"
         dram = int(4 * (2 * c.plane_size - 1) ** 2 * 8 + rows * c.plane_size * 8)
         rank_updates = job.stats()["updates"]
         achieved = rank_updates / (k_ms * 1e-3) if k_ms > 0 else None
@@ -559,12 +563,12 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
                                 "capture; dominated by the fixed-order fp32 partial-sum planes "
                                 "(compute-bound kernel, < 1% DRAM utilisation)")
     if bound == "fp32" and achieved:
-        # the packed-FFMA2 ceiling measured by tools/microbench_fmamix.cu on this
-        # pool (16 independent accumulators, no loads): 111 of 128 lane-FMA/clk/SM
+        # the packed-FFMA2 ceiling measured by tools/microbench_operands.cu on this
+        # pool for K4's operand form (uniform-register weight, no loads)
         ceil = SM_COUNT * f_max * FFMA2_CEILING_LANE_FMA_PER_CLK / 2.0
         roof["measured_ffma2_ceiling"] = ceil
         roof["frac_of_measured_ffma2_ceiling"] = achieved / ceil
-        roof["ffma2_ceiling_source"] = "profiles/s3_microbench_fmamix.txt"
+        roof["ffma2_ceiling_source"] = "profiles/s4_microbench_operands.txt"
     if bound == "sfu" and achieved:
         fp32_peak = SM_COUNT * f_max * 128.0 / K3_LANE_OPS_PER_UPDATE
         roof["fp32_bound"] = fp32_peak

@@ -48,6 +48,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     if lib.exists() and lib.stat().st_mtime >= newest and not force:
         return lib
     extra = ["-DWCGH_CHECKED"] if checked else []
+    # tuning builds only, e.g. WCGH_NVCC_EXTRA=-DWCGH_LUT_SWEEP (more K4 window shapes)
+    extra += os.environ.get("WCGH_NVCC_EXTRA", "").split()
 
     def one(src):
         obj = out_dir / (Path(src).stem + ".o")

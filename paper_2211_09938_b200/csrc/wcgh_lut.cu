@@ -480,14 +480,17 @@ __global__ void k_reduce_partials(const float2* __restrict__ partial, int n, siz
 constexpr int kMaxChunkSteps = 4096;
 
 // Register-window shape: R rows x PX columns per thread, D rows of prefetch,
-// W warps per CTA. Default 8 x 2 x 2 x 4; WCGH_LUT_VARIANT="R,PX,D,W" selects
-// another compiled shape (tuning only; results equal up to fp32 rounding).
+// W warps per CTA. Default 16 x 2 x 2 x 4 (168 registers, 12 warps/SM: one
+// LUT row segment feeds 32 FFMA2s, half the loads per MAC of the 8-row window;
+// config 2 K4 26.86 -> 25.14 ms, profiles/s5_k4_chunk_sweep.md);
+// WCGH_LUT_VARIANT="R,PX,D,W" selects another compiled shape (tuning only;
+// results equal up to fp32 rounding).
 struct LutVariant {
   int R, PX, D, W;
 };
 LutVariant lut_variant() {
   static const LutVariant v = [] {
-    LutVariant d{8, 2, 2, 4};
+    LutVariant d{16, 2, 2, 4};
     if (const char* e = std::getenv("WCGH_LUT_VARIANT"); e && *e) {
       int r = 0, px = 0, dd = 0, w = 4;
       const int got = std::sscanf(e, "%d,%d,%d,%d", &r, &px, &dd, &w);
@@ -500,7 +503,7 @@ LutVariant lut_variant() {
 // Largest gap (in cell rows) a run steps through with zero weights; a wider
 // gap starts a new run (window reload). WCGH_LUT_GAP overrides (tuning).
 int lut_gap() {
-  static const int g = std::max(1, env_int("WCGH_LUT_GAP", lut_variant().R));
+  static const int g = std::max(1, env_int("WCGH_LUT_GAP", std::min(4, lut_variant().R)));
   return g;
 }
 int lut_chunk_target() {
@@ -557,6 +560,17 @@ void launch_chunk_b(const LutVariant& v, const float2* lut, int nh, int off, int
   WCGH_V(8, 2, 1, 4)
   WCGH_V(8, 2, 3, 4)
   WCGH_V(16, 2, 2, 4)
+#ifdef WCGH_LUT_SWEEP
+  WCGH_V(16, 2, 1, 4)
+  WCGH_V(16, 2, 3, 4)
+  WCGH_V(12, 2, 2, 4)
+  WCGH_V(16, 1, 2, 4)
+  WCGH_V(16, 2, 2, 2)
+  WCGH_V(24, 1, 2, 2)
+  WCGH_V(32, 1, 2, 2)
+  WCGH_V(24, 2, 2, 2)
+  WCGH_V(20, 2, 2, 2)
+#endif
 #undef WCGH_V
   throw ValidationError("WCGH_LUT_VARIANT: shape not compiled for the chunk kernel");
 }
@@ -684,7 +698,10 @@ int launch_lut_chunks(const float2* lut, int nh, int block, const StageCells& sc
       WCGH_CUDA(cudaEventRecord(ss.join[k], ss.st[k]));
       WCGH_CUDA(cudaStreamWaitEvent(s, ss.join[k], 0));
     }
-    if (timing) WCGH_CUDA(cudaEventRecord(timing->end(), s));
+    if (timing) {
+      WCGH_CUDA(cudaEventRecord(timing->end(), s));
+      timing->extra += ng - 1;
+    }
     k_reduce_partials<<<unsigned((band + 255) / 256), 256, 0, s>>>(part, ng, band,
                                                                   accumulate || g0 > 0, rotate, out);
     WCGH_CHECK_LAUNCH();

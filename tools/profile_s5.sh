@@ -2,7 +2,7 @@
 # Session-5 K4 pass (parameter-block form, k_lut_chunk) at config 2, LUT method:
 #   1. launch list of the bench command (device time per launch);
 #   2. ncu --set full (+source) of two B = 1 chunk launches;
-#   3. window-shape / gap sweep of the chunk kernel (kernel ms, FP32 fraction).
+#   3. LUT-method bench lines at configs 2, 1 and 4 (kernel ms, FP32 fraction).
 # Every ncu command runs only after the identical plain command exited 0.
 set -u
 OUT=${OUT:-gpurun_out}; TAG=${TAG:-s5}
@@ -13,11 +13,12 @@ timeout 300 $B2 > "$OUT/plain2_$TAG.log" 2>&1 && \
     --log-file "$OUT/launches_cfg2_$TAG.csv" $B2 > "$OUT/ncu_l2_$TAG.log" 2>&1; echo "ncu_launch=$?"
 timeout 300 $B2 > "$OUT/plain2b_$TAG.log" 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on \
-    --kernel-name-base demangled -k "regex:k_lut_chunk<1," -s 6 -c 2 \
+    --kernel-name-base demangled -k "regex:k_lut_chunk<\\(int\\)1," -s 6 -c 2 \
     -o "$OUT/prof_k4chunk_$TAG" $B2 > "$OUT/ncu_k4chunk_$TAG.log" 2>&1; echo "ncu_k4=$?"
-for v in "8,2,2,4" "8,2,1,4" "8,2,3,4" "16,2,2,4"; do
-  for g in 8 4; do
-    r=$(WCGH_LUT_VARIANT=$v WCGH_LUT_GAP=$g timeout 300 python bench.py --config 2 --method lut --steps 5 --warmup 3 --no-cpu-baseline --no-extra 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('%.3f ms  kernel %.3f ms  frac %.4f' % (d['ms_per_step'], r['kernel_ms'], r['frac']))" 2>&1)
-    echo "variant=$v gap=$g cfg2 lut: $r"
-  done
-done | tee "$OUT/k4chunk_sweep_$TAG.txt"
+for cfg in 2 1 4; do
+  timeout 600 python bench.py --config $cfg --method lut --steps 5 --warmup 3 --no-cpu-baseline --no-extra > "$OUT/b${cfg}_lut_$TAG.json" 2> "$OUT/b${cfg}_lut_$TAG.err"
+  python -c "
+import json
+d=json.loads(open('$OUT/b${cfg}_lut_$TAG.json').read().strip().splitlines()[-1]); r=d['roofline']
+print('cfg$cfg lut: %.3f ms/holo  kernel %.3f ms  frac %.4f' % (d['ms_per_step'], r['kernel_ms'], r['frac']))"
+done | tee "$OUT/k4_lut_configs_$TAG.txt"
