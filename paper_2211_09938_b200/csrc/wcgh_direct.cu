@@ -475,7 +475,7 @@ __device__ __forceinline__ void rotate_chirp(float2 (&hr)[16], float2 (&hi)[16],
   }
 }
 
-template <int NC, int AMP, int MINB, bool CPLX, int RU>
+template <int NC, int AMP, int MINB, bool CPLX, int RU, int HOLD>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_direct_chirp(const int4* __restrict__ pts, const long long* __restrict__ layer_begin,
                  int n_layers, long long n_points, int chunk0, int nh, int row0, int rows,
@@ -547,6 +547,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const float2 tq2 = make_float2(4.0f * csq, 4.0f * csq);
     const float2 tq1 = make_float2((6.0f * L - 2.0f) * csq, (6.0f * L - 2.0f) * csq);
     const float2 tq0 = make_float2((1.5f * L * L - 1.0f) * csq, (1.5f * L * L - 1.0f) * csq);
+    const float2 hold_off = make_float2(-float(HOLD * HOLD) / 16.0f, -float(HOLD * HOLD) / 16.0f);
+    (void)hold_off;
     const float2 xscale = make_float2(kTwoPi / 2147483648.0f, kTwoPi / 2147483648.0f);  // 2pi / 2^31
     const float2 s3 = make_float2(-1.0f / 6.0f, -1.0f / 6.0f);
 
@@ -583,41 +585,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const float2 fx = make_float2(i2f_small(dxa), i2f_small(dxa + L));
         const float2 U = __fmul2_rn(make_float2(__int2float_rn(sa), __int2float_rn(sb)), cc);
 
-        // ---- seed w_0 (the fixed kernel's per-pixel evaluation)
-        float2 wr, wi;
-        {
-          const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
-                                         __int_as_float((tb >> 9) | 0x3f800000u));
-          const float2 u2 = __fmul2_rn(U, U);
-          float2 pc = corr[NC - 1];
-#pragma unroll
-          for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
-          const float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
-          const float a0 = __int_as_float(q.z);
-          const float2 A0 = make_float2(a0, a0);
-          float2 am;
-          if constexpr (AMP == 3) {
-            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2),
-                         A3 = make_float2(a0 * am3, a0 * am3);
-            am = __ffma2_rn(__ffma2_rn(__ffma2_rn(A3, U, A2), U, A1), U, A0);
-          } else if constexpr (AMP == 2) {
-            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2);
-            am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
-          } else if constexpr (AMP == 1) {
-            const float a1 = CPLX ? a0 * am1 : __int_as_float(q.w);
-            am = __ffma2_rn(make_float2(a1, a1), U, A0);
-          } else {
-            am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
-          }
-          float2 sn, cs;
-          __sincosf(ph.x, &sn.x, &cs.x);
-          __sincosf(ph.y, &sn.y, &cs.y);
-          wr = __fmul2_rn(am, cs);
-          wi = __fmul2_rn(am, sn);
-        }
-
         // ---- seed v_0 and its per-step increment g
-        float2 vr, vi, gr, gi;
+        float2 vr, vi, gr, gi, dcs;
         {
           const float2 du = __ffma2_rn(fx, c2, cc);      // u(x+1) - u(x) = c (2x + 1)
           const float2 um = __ffma2_rn(du, half2, U);    // u at x + 1/2
@@ -657,17 +626,57 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // relative at the end of a run) is dropped
           gr = __fmul2_rn(vi, make_float2(-dc.x, -dc.y));
           gi = __fmul2_rn(vr, dc);
+          dcs = dc;
         }
 
-        // z_i (w_i without the common chirp Q_i): z_{i+1} = z_i v_i, v_i = v_0 + i g
+        // ---- seed w_0 (the fixed kernel's per-pixel evaluation)
+        float2 wr, wi;
+        {
+          const float2 phf = make_float2(__int_as_float((ta >> 9) | 0x3f800000u),
+                                         __int_as_float((tb >> 9) | 0x3f800000u));
+          const float2 u2 = __fmul2_rn(U, U);
+          float2 pc = corr[NC - 1];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) pc = __ffma2_rn(pc, U, corr[k]);
+          float2 ph = __ffma2_rn(phf, two_pi2, __ffma2_rn(u2, pc, neg3pi2));
+          // a held multiplier leads the exact phase by dc t (HOLD - t) / 2 inside a
+          // sub-run (0 at its ends): centre that error, +- dc HOLD^2 / 16
+          if constexpr (HOLD > 1) ph = __ffma2_rn(dcs, hold_off, ph);
+          const float a0 = __int_as_float(q.z);
+          const float2 A0 = make_float2(a0, a0);
+          float2 am;
+          if constexpr (AMP == 3) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2),
+                         A3 = make_float2(a0 * am3, a0 * am3);
+            am = __ffma2_rn(__ffma2_rn(__ffma2_rn(A3, U, A2), U, A1), U, A0);
+          } else if constexpr (AMP == 2) {
+            const float2 A1 = make_float2(a0 * am1, a0 * am1), A2 = make_float2(a0 * am2, a0 * am2);
+            am = __ffma2_rn(__ffma2_rn(A2, U, A1), U, A0);
+          } else if constexpr (AMP == 1) {
+            const float a1 = CPLX ? a0 * am1 : __int_as_float(q.w);
+            am = __ffma2_rn(make_float2(a1, a1), U, A0);
+          } else {
+            am = make_float2(a0 * rsqrtf(1.0f + U.x), a0 * rsqrtf(1.0f + U.y));
+          }
+          float2 sn, cs;
+          __sincosf(ph.x, &sn.x, &cs.x);
+          __sincosf(ph.y, &sn.y, &cs.y);
+          wr = __fmul2_rn(am, cs);
+          wi = __fmul2_rn(am, sn);
+        }
+
+        // z_i (w_i without the common chirp Q_i): z_{i+1} = z_i v_i, v_i = v_0 + i g;
+        // HOLD > 1: one multiplier per sub-run of HOLD steps, the sub-run's mean
+        // v_0 + (s + (HOLD - 1) / 2) g (exact phase at the sub-run ends)
+        float2 ur = vr, ui = vi;
 #pragma unroll
         for (int i = 0; i < L; ++i) {
           hr[i] = __fadd2_rn(hr[i], wr);
           hi[i] = __fadd2_rn(hi[i], wi);
           if (i < L - 1) {
-            float2 ur = vr, ui = vi;
-            if (i > 0) {
-              const float2 fi = make_float2(float(i), float(i));
+            if (i % HOLD == 0 && (i > 0 || HOLD > 1)) {
+              const float f = float(i) + 0.5f * float(HOLD - 1);
+              const float2 fi = make_float2(f, f);
               ur = __ffma2_rn(gr, fi, vr);
               ui = __ffma2_rn(gi, fi, vi);
             }
@@ -855,26 +864,35 @@ int rec_unroll() {  // point loop unrolled by 2 (WCGH_DIRECT_RU=1: not unrolled,
   return env_int("WCGH_DIRECT_RU", 2) == 1 ? 1 : 2;
 }
 
+template <int NC, int AMP, bool CPLX, int RU, int HOLD>
+void launch_chirp(const LaunchArgs& a) {
+  constexpr int MINB = 2;
+  const size_t dyn = a.G > 1 ? kChirpAccBytes : 0;
+  // per device and cheap: set on every launch (multi-device callers)
+  if (dyn)
+    WCGH_CUDA(cudaFuncSetAttribute(k_direct_chirp<NC, AMP, MINB, CPLX, RU, HOLD>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(kChirpAccBytes)));
+  k_direct_chirp<NC, AMP, MINB, CPLX, RU, HOLD><<<a.grid, kThreads, dyn, a.s>>>(
+      a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride, a.G);
+}
+
 template <int NC, int AMP>
-void launch_rec(const LaunchArgs& a, bool chirp) {
+void launch_rec(const LaunchArgs& a, bool chirp, int hold) {
   constexpr int MINB = 2;
 #define WCGH_REC(CPLX_, RU_)                                                              \
-  if (chirp) {                                                                            \
-    const size_t dyn = a.G > 1 ? kChirpAccBytes : 0;                                      \
-    /* per device and cheap: set on every launch (multi-device callers) */                 \
-    if (dyn)                                                                              \
-      WCGH_CUDA(cudaFuncSetAttribute(k_direct_chirp<NC, AMP, MINB, CPLX_, RU_>,           \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                                     int(kChirpAccBytes)));                                \
-    k_direct_chirp<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, dyn, a.s>>>(           \
-        a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride, \
-        a.G);                                                                             \
-  } else                                                                                  \
+  if (chirp)                                                                              \
+    launch_chirp<NC, AMP, CPLX_, RU_, 1>(a);                                              \
+  else                                                                                    \
     k_direct_rec<NC, AMP, MINB, CPLX_, RU_><<<a.grid, kThreads, 0, a.s>>>(               \
         a.pts, a.lb, a.L, a.np, a.chunk0, a.nh, a.row0, a.rows, a.tiles_x, a.out, a.stride)
   const bool u2 = rec_unroll() == 2;
   if (a.cplx) {
     if (u2) WCGH_REC(true, 2); else WCGH_REC(true, 1);
+  } else if (chirp && u2 && hold == 4) {  // held multipliers: real amplitudes, default unroll
+    launch_chirp<NC, AMP, false, 2, 4>(a);
+  } else if (chirp && u2 && hold == 2) {
+    launch_chirp<NC, AMP, false, 2, 2>(a);
   } else {
     if (u2) WCGH_REC(false, 2); else WCGH_REC(false, 1);
   }
@@ -885,13 +903,13 @@ template <int NC>
 void launch_rec_amp(const DirectPlan& plan, const LaunchArgs& a) {
   const bool chirp = plan.rec == 2;
   if (plan.amp_degree == 1)
-    launch_rec<NC, 1>(a, chirp);
+    launch_rec<NC, 1>(a, chirp, plan.hold);
   else if (plan.amp_degree == 2)
-    launch_rec<NC, 2>(a, chirp);
+    launch_rec<NC, 2>(a, chirp, plan.hold);
   else if (plan.amp_degree == 3)
-    launch_rec<NC, 3>(a, chirp);
+    launch_rec<NC, 3>(a, chirp, plan.hold);
   else
-    launch_rec<NC, 0>(a, chirp);
+    launch_rec<NC, 0>(a, chirp, plan.hold);
 }
 
 void launch_rec_nc(const DirectPlan& plan, const LaunchArgs& a) {
@@ -1106,6 +1124,24 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
     bool small_dq = true;  // k_direct_rec expands the quadratic second difference
     for (int l = 0; l < n_layers; ++l) small_dq = small_dq && std::fabs(h_layers[l].dq) <= 0.03f;
     plan.rec = !ok || rec_env == 0 ? 0 : (rec_env == 1 ? (small_dq ? 1 : 0) : 2);
+    // Held run multipliers (k_direct_chirp, real amplitudes): the multiplier v_0 + i g
+    // is refreshed every `hold` steps with the sub-run's mean. Inside a sub-run the
+    // phase then deviates by dc t (hold - t) / 2, centred to +- dc hold^2 / 16 by the
+    // seed offset: hold = 4 (2) while that stays <= 1.5e-5 rad at the farthest
+    // (pixel, point) pair (configs 1, 3, 4: 7.1e-6, 1.2e-5, 7.1e-6 at hold 4; config
+    // 2: 7.1e-6 at hold 2). WCGH_DIRECT_HOLD = 1, 2 or 4 overrides (tuning).
+    plan.hold = 1;
+    if (plan.rec == 2 && !pim_dev) {
+      double dc_max = 0.0;
+      for (int l = 0; l < n_layers; ++l) {
+        const double G = 2.0 * 3.141592653589793 * layers[l].z / layers[l].wavelength;
+        const double cl = layers[l].pitch * layers[l].pitch / (layers[l].z * layers[l].z);
+        dc_max = std::max(dc_max, G * cl * cl * (3.0 * max_dx * max_dx + max_dy * max_dy) / 2.0);
+      }
+      constexpr double kHoldTol = 1.5e-5;
+      plan.hold = dc_max <= kHoldTol ? 4 : (dc_max / 4.0 <= kHoldTol ? 2 : 1);
+      if (const int h = env_int("WCGH_DIRECT_HOLD", 0); h == 1 || h == 2 || h == 4) plan.hold = h;
+    }
   }
   WCGH_CUDA(cudaMemcpyToSymbolAsync(c_layers, h_layers, sizeof(DirectLayer) * n_layers, 0,
                                     cudaMemcpyHostToDevice, stream));

@@ -201,6 +201,7 @@ struct DirectPlan {
   double u_max;
   int rec;         // 0 per-pixel (k_direct_fixed); angle-addition recurrence along
                    // 16-pixel runs: 1 k_direct_rec, 2 chirp-factored k_direct_chirp
+  int hold = 1;    // k_direct_chirp: steps the run multiplier is held for (1, 2 or 4)
 };
 
 // CUDA-event pairs around each launch of a kernel family (for per-kernel

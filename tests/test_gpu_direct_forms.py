@@ -183,3 +183,20 @@ def test_direct_random_geometries(ctx, case):
                           py.ravel()).reshape(len(rows), nh)
     err = O.rel_l2(got, ref)
     assert err <= 1e-5, (case, nh, pitch, zs, err)
+
+
+@pytest.mark.parametrize("hold", ["1", "2", "4"])
+def test_chirp_held_multipliers(ctx, monkeypatch, reference, hold):
+    """k_direct_chirp refreshes the run multiplier v_0 + i g every HOLD steps
+    (the planner picks 4, 2 or 1 from the worst-case curvature; forced here).
+    Each setting stays within 1e-5 of the fp64 Eq.(1) oracle on the two-layer
+    1500-wide case, and the settings agree with each other to the fp32 level
+    of the error the hold introduces (<= dc HOLD^2 / 16 rad per contribution)."""
+    pts, ref = reference
+    monkeypatch.setenv("WCGH_DIRECT_REC", "2")
+    monkeypatch.setenv("WCGH_DIRECT_HOLD", hold)
+    got = np.stack([stages.synth_points(pts, LAYERS, NH, row0=r, rows=1)[0] for r in ROWS])
+    assert O.rel_l2(got, ref) <= 1e-5, (hold, O.rel_l2(got, ref))
+    monkeypatch.setenv("WCGH_DIRECT_HOLD", "1")
+    base = np.stack([stages.synth_points(pts, LAYERS, NH, row0=r, rows=1)[0] for r in ROWS])
+    assert O.rel_l2(got, base) <= 5e-6, (hold, O.rel_l2(got, base))
