@@ -43,11 +43,13 @@ UNIT = "updates/s"
 SM_COUNT = 148
 MUFU_PER_CLK_SM = 16.0
 CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
-# K3 as built (k_direct_chirp, point loop unrolled by 2): per point and thread
-# (32 updates) 154 packed fp32x2 FMA-pipe instructions (config 4, NC = 3) +
-# ~10 scalar FMA-pipe ones -> ~10 FP32 lane operations per update.
+# K3 as built (k_direct_chirp, NC = 3, point loop unrolled by 2): FMA-pipe lane
+# operations per update counted from the SASS of the point loop (2 points x 32
+# pixels = 64 updates per trip): multiplier held for 1 / 2 / 4 steps = 308 / 286 /
+# 270 packed fp32x2 instructions + 28 / 27 / 27 scalar FMA-pipe ones
+# (profiles/sass/k3_direct_chirp_NC3_AMP1_RU2[_HOLD2|_HOLD4].sass).
 K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
-K3_LANE_OPS_PER_UPDATE = 10.0
+K3_LANE_OPS_BY_HOLD = {1: 10.06, 2: 9.36, 4: 8.86}
 # packed FFMA2 with the scalar operand in a uniform register (K4's parameter-block form),
 # measured by tools/microbench_operands.cu: profiles/s4_microbench_operands.txt (116 of 128;
 # 111 with the weight in a regular register, 125-127 straight from the constant bank)
@@ -514,13 +516,15 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
     achieved = rank_updates / (k_ms * 1e-3) if k_ms > 0 else None
     if job.spec.method == "direct":
         per_clk, kernel = MUFU_PER_CLK_SM / CANON_SFU_PER_UPDATE, K3_KERNEL
+        form, hold = job.direct_form()
+        lane_ops = K3_LANE_OPS_BY_HOLD.get(hold if form == 2 else 1, 10.06)
         basis = (f"canonical SFU roofline {SM_COUNT} SMs x {f_max/1e6:.0f} MHz (MEASURED_PEAKS "
                  "sm_max_mhz) x 16 MUFU/clk/SM / 3 MUFU per update (SURVEY.md §8(d)). K3 "
                  "evaluates exp(ikr)/r by angle addition along 16-pixel runs (2 MUFU per run "
                  "seed, 4 per 32 updates), so it is bound by the FP32 pipe instead: "
                  "frac_of_fp32_bound = achieved / (148 x f x 128 lane-ops/clk/SM / "
-                 f"{K3_LANE_OPS_PER_UPDATE} lane-ops per update, counted from the SASS in "
-                 "profiles/sass/k3_direct_chirp_NC3_AMP1_RU2.sass); not an HBM or tensor-core kernel")
+                 f"{lane_ops} lane-ops per update at hold = {hold}, counted from the SASS in "
+                 "profiles/sass/k3_direct_chirp_NC3_AMP1_RU2*.sass); not an HBM or tensor-core kernel")
         bound, key = "sfu", "k_direct_chirp"
         dram = int(points * 16 + rows * c.plane_size * 8)
     elif job.spec.method == "lut":
@@ -570,10 +574,11 @@ def _roofline(job, c, points, rows, k_ms, f_max, f_meas, workload):
         roof["frac_of_measured_ffma2_ceiling"] = achieved / ceil
         roof["ffma2_ceiling_source"] = "profiles/s4_microbench_operands.txt"
     if bound == "sfu" and achieved:
-        fp32_peak = SM_COUNT * f_max * 128.0 / K3_LANE_OPS_PER_UPDATE
+        fp32_peak = SM_COUNT * f_max * 128.0 / lane_ops
         roof["fp32_bound"] = fp32_peak
         roof["frac_of_fp32_bound"] = achieved / fp32_peak
-        roof["fp32_lane_ops_per_update"] = K3_LANE_OPS_PER_UPDATE
+        roof["fp32_lane_ops_per_update"] = lane_ops
+        roof["k3_form"] = {"form": form, "hold": hold}
     return roof
 
 
@@ -763,6 +768,7 @@ def measure(sc, method, args, ctx, stream, world, rank, local, flush, extras):
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t / e2e_steps, "steps": e2e_steps,
+                "step_ms": [round(v, 3) for v in e2e_ms],
                 "warmup": e2e_warm,
                 "path": ("HologramJob.upload (H2D from pinned host) -> run -> download (D2H of the "
                          "whole assembled plane, rank 0) through the C ABI")},

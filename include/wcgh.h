@@ -310,6 +310,12 @@ int wcgh_job_download_stages(wcgh_job* job, float* out4);
 /* Device pointer of the row band (rows x Nh complex64), valid until destroy. */
 void* wcgh_job_plane_dev(wcgh_job* job);
 int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out);
+/* Which K3 form the last direct-method run launched (tuning and the bench's
+ * roofline; no reference counterpart): form 0 per-pixel, 1 recurrence,
+ * 2 chirp-factored recurrence, 3 fp64 phase, -1 before the first run (or an
+ * empty point list); hold = steps a run multiplier is held for (1, 2 or 4;
+ * form 2 only). */
+int wcgh_job_direct_form(const wcgh_job* job, int* form, int* hold);
 
 /* Replaces random_phase_field (synthesis.hpp:101-104, synthesis.cpp:288-296):
  * out[i] = polar(amplitude[i], U[0, 2pi)) with std::mt19937_64(seed) drawn

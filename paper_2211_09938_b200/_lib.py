@@ -102,6 +102,7 @@ _SIGS = [
     ("wcgh_job_download_stages", C.c_int, [_VP, _VP]),
     ("wcgh_job_plane_dev", _VP, [_VP]),
     ("wcgh_job_stats", C.c_int, [_VP, C.POINTER(Stats)]),
+    ("wcgh_job_direct_form", C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("wcgh_write_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int, C.POINTER(Layer)]),
     ("wcgh_read_cgh1", C.c_int, [C.c_char_p, _VP, C.c_int64, C.POINTER(C.c_int), C.POINTER(Layer)]),
     ("wcgh_job_write_cgh1", C.c_int, [_VP, C.c_char_p, C.c_int]),

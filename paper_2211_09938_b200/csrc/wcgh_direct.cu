@@ -1143,6 +1143,10 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
       if (const int h = env_int("WCGH_DIRECT_HOLD", 0); h == 1 || h == 2 || h == 4) plan.hold = h;
     }
   }
+  if (timing) {
+    timing->form = phase_mode == WCGH_PHASE_FIXED ? plan.rec : 3;
+    timing->hold = plan.hold;
+  }
   WCGH_CUDA(cudaMemcpyToSymbolAsync(c_layers, h_layers, sizeof(DirectLayer) * n_layers, 0,
                                     cudaMemcpyHostToDevice, stream));
 

@@ -210,6 +210,7 @@ struct DirectTiming {
   std::vector<cudaEvent_t> ev;
   size_t used = 0;
   int extra = 0;  // launches inside timed intervals beyond one each (K4 chunk launches)
+  int form = -1, hold = 0;  // launch_direct's choice for the last run (DirectPlan::rec, ::hold)
   cudaEvent_t next() {
     if (used == ev.size()) {
       cudaEvent_t e;

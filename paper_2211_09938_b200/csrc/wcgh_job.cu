@@ -652,6 +652,15 @@ int wcgh_job_stats(const wcgh_job* job, wcgh_stats* out) {
   });
 }
 
+int wcgh_job_direct_form(const wcgh_job* job, int* form, int* hold) {
+  return guard(job ? job->ctx : nullptr, [&] {
+    require(job && form && hold, "job_direct_form: NULL argument");
+    require(job->desc.method == WCGH_METHOD_DIRECT, "job_direct_form: the job does not use the direct method");
+    *form = job->timing.form;
+    *hold = job->timing.hold;
+  });
+}
+
 int wcgh_job_load_lut(wcgh_job* job, int layer, int block, const float* lut) {
   return guard(job ? job->ctx : nullptr, [&] {
     require(job && lut, "job_load_lut: NULL argument");

@@ -187,6 +187,13 @@ class HologramJob:
             "total_launches": s.total_launches,
         }
 
+    def direct_form(self) -> tuple:
+        """(form, hold) of the K3 kernel the last direct-method run launched
+        (0 per-pixel, 1 recurrence, 2 chirp-factored recurrence, 3 fp64 phase)."""
+        f, h = C.c_int(-1), C.c_int(0)
+        L.check(self.ctx.lib.wcgh_job_direct_form(self.h, C.byref(f), C.byref(h)))
+        return int(f.value), int(h.value)
+
     def __call__(self, objects: np.ndarray, saliency: np.ndarray) -> np.ndarray:
         self.upload(objects, saliency)
         self.run()
