@@ -200,3 +200,31 @@ def test_chirp_held_multipliers(ctx, monkeypatch, reference, hold):
     monkeypatch.setenv("WCGH_DIRECT_HOLD", "1")
     base = np.stack([stages.synth_points(pts, LAYERS, NH, row0=r, rows=1)[0] for r in ROWS])
     assert O.rel_l2(got, base) <= 5e-6, (hold, O.rel_l2(got, base))
+
+
+def test_job_reports_direct_form(ctx, monkeypatch):
+    """wcgh_job_direct_form: the K3 form and hold the last direct run launched
+    (config 1's geometry: chirp-factored recurrence, multiplier held for 4
+    steps; WCGH_DIRECT_REC=0: the per-pixel form; the fp64 phase mode: 3)."""
+    from paper_2211_09938_b200 import scenes
+    from paper_2211_09938_b200.hologram import HologramJob, spec_for_scene
+
+    for name in ("WCGH_DIRECT_REC", "WCGH_DIRECT_HOLD"):
+        monkeypatch.delenv(name, raising=False)
+    sc = scenes.make_scene(1)
+    job = HologramJob(spec_for_scene(sc, method="direct", row0=0, rows=8))
+    assert job.direct_form() == (-1, 0)  # nothing launched yet
+    job.upload(sc.objects, sc.masks)
+    job.run()
+    assert job.direct_form() == (2, 4)
+    monkeypatch.setenv("WCGH_DIRECT_HOLD", "2")
+    job.run()
+    assert job.direct_form() == (2, 2)
+    monkeypatch.setenv("WCGH_DIRECT_REC", "0")
+    job.run()
+    assert job.direct_form()[0] == 0
+    job.close()
+    lut = HologramJob(spec_for_scene(sc, method="lut", row0=0, rows=8))
+    with pytest.raises(_lib.ValidationError):
+        lut.direct_form()
+    lut.close()
