@@ -45,11 +45,11 @@ MUFU_PER_CLK_SM = 16.0
 CANON_SFU_PER_UPDATE = 3.0  # rsqrt, sin, cos
 # K3 as built (k_direct_chirp, NC = 3, point loop unrolled by 2): FMA-pipe lane
 # operations per update counted from the SASS of the point loop (2 points x 32
-# pixels = 64 updates per trip): multiplier held for 1 / 2 / 4 steps = 308 / 286 /
-# 270 packed fp32x2 instructions + 28 / 27 / 27 scalar FMA-pipe ones
+# pixels = 64 updates per trip): multiplier held for 1 / 2 / 4 steps = 308 / 282 /
+# 266 packed fp32x2 instructions + 28 / 28 / 27 scalar FMA-pipe ones
 # (profiles/sass/k3_direct_chirp_NC3_AMP1_RU2[_HOLD2|_HOLD4].sass).
 K3_KERNEL = "k_direct_chirp (K3, chirp-factored angle-addition recurrence)"
-K3_LANE_OPS_BY_HOLD = {1: 10.06, 2: 9.36, 4: 8.86}
+K3_LANE_OPS_BY_HOLD = {1: 10.06, 2: 9.25, 4: 8.73}
 # packed FFMA2 with the scalar operand in a uniform register (K4's parameter-block form),
 # measured by tools/microbench_operands.cu: profiles/s4_microbench_operands.txt (116 of 128;
 # 111 with the weight in a regular register, 125-127 straight from the constant bank)
@@ -164,9 +164,11 @@ class ClockSampler:
             for name, v in zip(names, s[4:8]):
                 if v.lower() == "active":
                     reasons.add(name)
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "sm_min_mhz": min(sm) if sm else None,
+                "power_w_median": float(np.median(pw)) if pw else None}
 
 
 # ---------------------------------------------------------------------------
@@ -735,6 +737,8 @@ def measure(sc, method, args, ctx, stream, world, rank, local, flush, extras):
     if world > 1:
         dist.barrier()
     e2e_ms = []
+    e2e_clocks = ClockSampler(local)
+    e2e_clocks.start()
     for i in range(e2e_warm + e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -743,6 +747,7 @@ def measure(sc, method, args, ctx, stream, world, rank, local, flush, extras):
         torch.cuda.synchronize()
         if i >= e2e_warm:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_clk = e2e_clocks.stop()
     e2e_t = _max_over_ranks(float(np.sum(e2e_ms)), world)
     e2e_value = updates / (e2e_t / e2e_steps * 1e-3)
     h2d = int(sc.objects.nbytes + sc.masks.nbytes)
@@ -768,7 +773,7 @@ def measure(sc, method, args, ctx, stream, world, rank, local, flush, extras):
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t / e2e_steps, "steps": e2e_steps,
-                "step_ms": [round(v, 3) for v in e2e_ms],
+                "step_ms": [round(v, 3) for v in e2e_ms], "clocks": e2e_clk,
                 "warmup": e2e_warm,
                 "path": ("HologramJob.upload (H2D from pinned host) -> run -> download (D2H of the "
                          "whole assembled plane, rank 0) through the C ABI")},

@@ -545,8 +545,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
                                     -12582912.0f * (kTwoPi / 2147483648.0f));
     const float csq = c * c;
     const float2 tq2 = make_float2(4.0f * csq, 4.0f * csq);
-    const float2 tq1 = make_float2((6.0f * L - 2.0f) * csq, (6.0f * L - 2.0f) * csq);
-    const float2 tq0 = make_float2((1.5f * L * L - 1.0f) * csq, (1.5f * L * L - 1.0f) * csq);
+    // v is seeded at the middle of the first sub-run (x + HOLD / 2): T below is taken
+    // relative to that point (HOLD = 1: the historical constants, 0.5 c^2 apart)
+    const float tq1s = (6.0f * L - 2.0f * HOLD) * csq;
+    const float tq0s = (HOLD > 1 ? 1.5f * L * L - 0.5f * HOLD * HOLD : 1.5f * L * L - 1.0f) * csq;
+    const float2 tq1 = make_float2(tq1s, tq1s);
+    const float2 tq0 = make_float2(tq0s, tq0s);
+    const float2 chold = make_float2(float(HOLD) * c, float(HOLD) * c);
+    const float2 hhalf2 = make_float2(0.5f * HOLD, 0.5f * HOLD);
     const float2 hold_off = make_float2(-float(HOLD * HOLD) / 16.0f, -float(HOLD * HOLD) / 16.0f);
     (void)hold_off;
     const float2 xscale = make_float2(kTwoPi / 2147483648.0f, kTwoPi / 2147483648.0f);  // 2pi / 2^31
@@ -588,8 +594,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // ---- seed v_0 and its per-step increment g
         float2 vr, vi, gr, gi, dcs;
         {
-          const float2 du = __ffma2_rn(fx, c2, cc);      // u(x+1) - u(x) = c (2x + 1)
-          const float2 um = __ffma2_rn(du, half2, U);    // u at x + 1/2
+          // HOLD = 1: u(x+1) - u(x) = c (2x + 1) and u at x + 1/2; HOLD > 1: the mean
+          // first difference of the first sub-run, c (2x + HOLD), and u at its middle
+          // x + HOLD / 2 (to c HOLD^2 / 4 <= 2e-9), so v_0 is that sub-run's multiplier
+          const float2 du = __ffma2_rn(fx, c2, chold);
+          const float2 um = __ffma2_rn(du, hhalf2, U);
           float2 gq = dcorr[NC - 1], gpp = ddcorr[NC - 1];
 #pragma unroll
           for (int k = NC - 2; k >= 0; --k) {
@@ -618,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // the correction's second difference at the run's middle x + L/2:
           //   dc = G h''(u_m) u'(x+L/2)^2 + 2c G h'(u(x+L/2)),  G h'(u(x+L/2)) =
           //   gp + gpp (u(x+L/2) - um), which folds to gpp T + 2c gp with
-          //   T = u'(x+L/2)^2 + 2c (u(x+L/2) - um) = c^2 (4x^2 + (6L-2)x + 1.5L^2 - 1)
+          //   T = u'(x+L/2)^2 + 2c (u(x+L/2) - um) = c^2 (4x^2 + (6L-2H)x + 1.5L^2 - H^2/2)
           const float2 T = __ffma2_rn(fx, __ffma2_rn(fx, tq2, tq1), tq0);
           const float2 dc = __ffma2_rn(gpp, T, __fmul2_rn(gp, c2));
           // g = i dc v_0: v_i = v_0 (1 + sigma_c)^i = v_0 + i g + O(i^2 dc^2); the
@@ -667,15 +676,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
         // z_i (w_i without the common chirp Q_i): z_{i+1} = z_i v_i, v_i = v_0 + i g;
         // HOLD > 1: one multiplier per sub-run of HOLD steps, the sub-run's mean
-        // v_0 + (s + (HOLD - 1) / 2) g (exact phase at the sub-run ends)
+        // (exact phase at the sub-run ends): v_0 is the first sub-run's (seeded at
+        // its middle), the sub-run starting at step s takes v_0 + s g
         float2 ur = vr, ui = vi;
 #pragma unroll
         for (int i = 0; i < L; ++i) {
           hr[i] = __fadd2_rn(hr[i], wr);
           hi[i] = __fadd2_rn(hi[i], wi);
           if (i < L - 1) {
-            if (i % HOLD == 0 && (i > 0 || HOLD > 1)) {
-              const float f = float(i) + 0.5f * float(HOLD - 1);
+            if (i % HOLD == 0 && i > 0) {
+              const float f = float(i);
               const float2 fi = make_float2(f, f);
               ur = __ffma2_rn(gr, fi, vr);
               ui = __ffma2_rn(gi, fi, vi);
