@@ -1151,6 +1151,7 @@ int launch_direct(const wcgh_point* pts_dev, const int64_t* layer_begin_host, in
       constexpr double kHoldTol = 1.5e-5;
       plan.hold = dc_max <= kHoldTol ? 4 : (dc_max / 4.0 <= kHoldTol ? 2 : 1);
       if (const int h = env_int("WCGH_DIRECT_HOLD", 0); h == 1 || h == 2 || h == 4) plan.hold = h;
+      if (rec_unroll() != 2) plan.hold = 1;  // the held forms exist for the unrolled loop only
     }
   }
   if (timing) {
