@@ -244,10 +244,11 @@ void run_job_direct(wcgh_job* j, cudaStream_t s, bool synth) {
     j->stats.ms_total = j->stats.ms_analysis;
     return;
   }
-  // geometry bound on |dx|, |dy| for the phase-series plan
+  // geometry bound on |dx|, |dy| for the phase-series plan: the FULL plane's, never the
+  // band's, so every rank picks the same series lengths, kernel form and hold as a
+  // single-GPU run and its band stays bitwise equal to those rows of the whole plane
   const double far = double(j->off + No - 1);
-  const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
-                                 std::fabs(double(d.row0 + d.rows - 1) - j->off));
+  const double max_dy = std::max(far, double(d.plane_size - 1 - j->off));
   int launches = 0;
   if (fft) {
     // same hologram by FFT correlation; `updates` keeps the direct-sum count
@@ -435,8 +436,7 @@ void compute_stage_planes(wcgh_job* j, cudaStream_t s) {
   const size_t per_layer = size_t(No) * seg_per_row(No);
   const size_t nseg = per_layer * L;
   const double far = double(j->off + No - 1);
-  const double max_dy = std::max(std::fabs(double(d.row0) - (j->off + No - 1)),
-                                 std::fabs(double(d.row0 + d.rows - 1) - j->off));
+  const double max_dy = std::max(far, double(d.plane_size - 1 - j->off));  // full plane (see run)
   const bool cplx = j->complex_obj();
   float* img_im = cplx ? static_cast<float*>(j->snap_img_im.reserve(sizeof(float) * j->in_elems * L)) : nullptr;
   float* pim = cplx ? static_cast<float*>(j->snap_points_im.reserve(sizeof(float) * (j->in_elems * L + 1)))

@@ -236,3 +236,33 @@ def test_job_reports_direct_form(ctx, monkeypatch):
     with pytest.raises(_lib.ValidationError):
         lut.direct_form()
     lut.close()
+
+
+def test_band_plan_follows_the_full_plane(ctx, monkeypatch):
+    """The direct plan (series lengths, K3 form, hold) comes from the FULL
+    plane's geometry, never the row band's: at z = 0.1497 m (4 um pitch,
+    2048^2 on 4096^2) the whole plane's worst-case curvature allows hold 2
+    while a middle band on its own would allow hold 4. The band must launch
+    the full plane's form and equal those rows of the whole plane bitwise."""
+    from paper_2211_09938_b200.hologram import HologramJob, JobSpec
+
+    for name in ("WCGH_DIRECT_REC", "WCGH_DIRECT_HOLD", "WCGH_DIRECT_RU"):
+        monkeypatch.delenv(name, raising=False)
+    no, nh = 2048, 4096
+    rng = np.random.default_rng(5)
+    obj = np.zeros((1, no, no), np.uint8)
+    obj[0, rng.integers(0, no, 1500), rng.integers(0, no, 1500)] = rng.integers(1, 256, 1500)
+    obj[0, 0, 0] = obj[0, no - 1, no - 1] = obj[0, 0, no - 1] = 200
+    sal = np.full((1, no, no), 255, np.uint8)
+    layers = [(532e-9, 4e-6, 0.1497)]
+    whole = HologramJob(JobSpec(object_size=no, plane_size=nh, layers=layers, method="direct"))
+    full = whole(obj, sal)
+    assert whole.direct_form() == (2, 2)
+    whole.close()
+    for row0, rows in ((2040, 16), (0, 8), (4088, 8)):
+        band = HologramJob(JobSpec(object_size=no, plane_size=nh, layers=layers, method="direct",
+                                   row0=row0, rows=rows))
+        got = band(obj, sal)
+        assert band.direct_form() == (2, 2), (row0, band.direct_form())
+        assert np.array_equal(got, full[row0:row0 + rows]), row0
+        band.close()
