@@ -862,7 +862,9 @@ def main():
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        backend = os.environ.get("WCGH_BENCH_BACKEND", "nccl")
+        # NCCL refuses two ranks on one device, so the same-device check
+        # rendezvouses over gloo unless told otherwise
+        backend = os.environ.get("WCGH_BENCH_BACKEND", "gloo" if same_dev else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
